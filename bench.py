@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 implicit-LSKUM hot path (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): NACA 0012 O-grid 1280x500 (640,000
+points, radius 20), M 0.85, AoA 1 deg, modified LU-SGS with exact-AD JVPs
+(manish_ad), CFL 0.2, 3 inner gradient passes, physical BCs. A *step* is one
+fixed-point iteration (driver.cpp:218-276): q, 3 q-derivative passes, split-
+flux residual, time step + S-term + diagonal, 4 forward and 3 backward colour
+sweeps, update + BCs, residual norm and CL/CD.
+
+The reference aborts this case during iteration 22, so a
+long trajectory cannot be timed. Every timed step therefore re-runs iteration
+6 from the resident iteration-5 state (kf_bench_mode: the restart copy of U
+and dU_prev is inside the timed step).
+
+  value : device-timed Mpoint-iter/s (CUDA events on the library stream,
+          state resident in HBM), whole job over all ranks.
+  e2e   : the same metric through the reference-facing C-ABI call
+          kf_step_host with pinned HOST buffers: H2D(U, dU_prev) + iteration +
+          D2H(U', dU, record) every step.
+
+Multi-GPU (--gpus N under torchrun): "replicas only" for now — each rank
+solves its own copy of the cloud (weak scaling, no data-path collective);
+the partitioned solver with halo exchange is future work.
+
+--impl reference times the reference's own CPU solver (oracle/_ref, all host
+threads) on the same case.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CASE = dict(digits="0012", n_wall=1280, n_radial=500, radius=20.0, mach=0.85, aoa=1.0, cfl=0.2,
+            variant="manish_ad")
+METRIC = "Mpoint-iter/s (FP64 LU-SGS+AD) and time-to-residual-drop, NACA 0012 clouds"
+UNIT = "Mpoint-iter/s"
+WARM_ITERS = 5
+# algorithmic bytes of the flux-residual kernel per point
+# (q 32 + qx,qy 64 + xy 16 + ids 4*n_s + R 32, n_s = split entries with w != 0)
+FLUX_BYTES_FIXED = 144.0
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_cpu(n_iters_total, threads, spec=CASE):
+    """Time the reference solver (oracle/_ref, else the C restatement) on the
+    case. Returns (per-iteration seconds excluding each run's iteration 1,
+    N, kind). Runs restart from freestream before the reference's abort
+    (iteration 22) so any number of iterations can be sampled."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refpy  # checker: only the cpu_baseline / reference arm may use it
+    kind = "reference" if refpy.ref_available() else "port"
+    if kind == "reference":
+        refpy.Reference.num_threads(threads)
+        ctx = refpy.Reference.generate(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
+    else:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+        import paper_2406_07441_b200 as kf
+        c = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
+        nb = c.nbr
+        ctx = refpy.Oracle(c.x, c.y, c.kind, c.normal_x, c.normal_y, nb.offsets, nb.ids)
+    secs = []
+    while len(secs) < n_iters_total:
+        m = min(n_iters_total - len(secs) + 1, 20)
+        t0 = time.perf_counter()
+        r = ctx.run(variant=spec["variant"], n_iterations=m, mach=spec["mach"], aoa_deg=spec["aoa"],
+                    cfl=spec["cfl"])
+        wall = time.perf_counter() - t0
+        s = list(r.seconds[1:]) if kind == "reference" else [wall / max(len(r.residual), 1)] * (len(r.residual) - 1)
+        if not s:
+            break
+        secs.extend(s)
+    return secs[:n_iters_total], ctx.n, kind
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = cpu_cores()
+    secs, n, kind = reference_cpu(args.warmup + args.steps, threads)
+    timed = secs[args.warmup:args.warmup + args.steps] or secs
+    total = float(np.sum(timed))
+    value = n * len(timed) / total / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(timed), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(timed),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated NACA 0012 O-grid, deterministic)",
+        "config": {"workload": "naca0012:1280:500:20 M0.85 AoA1 manish_ad CFL0.2, one fixed-point iteration",
+                   "points": n, "parallelism": "cpu-openmp"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{len(timed)} reference iterations of the same case (runs restarted "
+                                   f"from freestream every <=19 iterations; iteration 1 of each run excluded)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="run a few steps for ncu (no JSON line)")
+    ap.add_argument("--points", default=None, help="override cloud n_wall:n_radial")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import paper_2406_07441_b200 as kf
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = dict(CASE)
+    if args.points:
+        nw, nr = args.points.split(":")
+        spec["n_wall"], spec["n_radial"] = int(nw), int(nr)
+
+    cloud = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
+    N = cloud.n()
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(spec["variant"]), mach_inf=spec["mach"],
+                          aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=64, device=local)
+    solver = kf.Solver(cloud, cfg)
+    solver.reset()
+    solver.iterate_async(WARM_ITERS)
+    recs, st = solver.sync_records()
+    assert st.code == 0 and len(recs) == WARM_ITERS, st.reason
+    solver.bench_mode(True)
+    stream = torch.cuda.ExternalStream(solver.stream_ptr, device=torch.device("cuda", local))
+
+    if args.profile_only:
+        solver.iterate_async(args.warmup + args.steps)
+        solver.sync_records()
+        torch.cuda.synchronize()
+        return 0
+
+    # ---- device-timed steps
+    solver.iterate_async(args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(stream)
+    solver.iterate_async(args.steps)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = t0.elapsed_time(t1)
+    recs, st = solver.sync_records()
+    if st.code != 0:
+        raise RuntimeError("benchmark iteration failed: " + st.reason.decode())
+    ms_t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = N * args.steps * world / (ms_max * 1e-3) / 1e6
+    launches = solver.launches_per_iteration * args.steps
+
+    # ---- end to end through the C ABI with pinned host buffers
+    U0, dU0 = solver.get_state(with_dU=True)
+    solver.bench_mode(True)
+    Uh = torch.from_numpy(U0).pin_memory()
+    dUh = torch.from_numpy(dU0).pin_memory()
+    Uo = torch.empty_like(Uh).pin_memory()
+    dUo = torch.empty_like(dUh).pin_memory()
+    import ctypes as C
+    from paper_2406_07441_b200 import _lib
+    rec = _lib.IterRecord()
+    h = solver._h
+
+    def e2e_step():
+        s = _lib.lib.kf_step_host(h, C.c_void_p(Uh.data_ptr()), C.c_void_p(dUh.data_ptr()),
+                                  C.c_void_p(Uo.data_ptr()), C.c_void_p(dUo.data_ptr()), C.byref(rec))
+        if s.code != 0:
+            raise RuntimeError(s.reason.decode())
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    e2e_ms = max(e0.elapsed_time(e1), 1e3 * wall)
+    et = torch.tensor([e2e_ms], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = N * args.steps * world / (float(et.item()) * 1e-3) / 1e6
+
+    # ---- per-kernel profile (CUDA events between launches) for the roofline
+    prof = solver.profile_kernels(reps=5)
+    total_ms = sum(t for _, t in prof)
+    agg = {}
+    for name, t in prof:
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += t
+    flux_ms = agg["flux_residual"][1]
+    ls = kf.build_ls_coefficients(cloud)
+    n_s = float(sum(np.count_nonzero(ls.split_w[k]) for k in ls.split_w)) / N
+    flux_bytes = N * (FLUX_BYTES_FIXED + 4.0 * n_s)
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    if not hbm_peak:
+        hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    achieved = flux_bytes / (flux_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "flux_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            if tj.get("points") == N:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    fp64_peak = kf.measure_fp64_peak(local)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
+        "config": {
+            "workload": "naca0012:1280:500:20 M0.85 AoA1 manish_ad CFL0.2 n_inner3, one fixed-point "
+                        "iteration (re-run of iteration 6 from the resident iteration-5 state)",
+            "points": N, "colours": int(kf.color_points(cloud).n_colors),
+            "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+            "l2": "inputs larger than L2 (per-iteration working set > 400 MB vs 126 MB L2)",
+        },
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(Uh.numel() * 8 + dUh.numel() * 8),
+                "d2h_bytes_per_step": int(Uo.numel() * 8 + dUo.numel() * 8 + C.sizeof(rec)),
+                "call": "kf_step_host (C ABI, pinned host buffers)"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "roofline": {
+            "bound": "hbm", "kernel": "flux_residual", "achieved": achieved, "peak": hbm_peak,
+            "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+            "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": flux_bytes,
+            "kernel_ms": flux_ms, "kernel_share_of_step": flux_ms / total_ms if total_ms else None,
+            "note": "the flux kernel is FP64-pipe bound (SURVEY.md F4); see fp64",
+            "fp64_peak_tflops_measured": fp64_peak,
+        },
+        "kernels_ms": {k: {"launches": v[0], "ms": v[1]} for k, v in agg.items()},
+        "check": {"residual": recs[WARM_ITERS].residual if len(recs) > WARM_ITERS else None,
+                  "cl": recs[WARM_ITERS].cl if len(recs) > WARM_ITERS else None},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        secs, n_ref, kind = reference_cpu(8, cpu_cores())
+        secs = secs[1:] or secs
+        line["cpu_baseline"] = {
+            "value": n_ref / float(np.median(secs)) / 1e6, "unit": UNIT, "cores": cpu_cores(),
+            "kind": kind, "sample": f"{len(secs)} iterations of the same case on the host "
+                                    "(median per-iteration time, warm-up iteration excluded)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

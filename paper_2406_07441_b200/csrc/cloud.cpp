@@ -1,0 +1,587 @@
+// Host-side ingestion. See cloud.hpp. Formulas follow the reference in
+// evaluation order (compiled with -ffp-contract=off, no -march) so that the
+// generated geometry, split stencils, LS weights and colours are bitwise the
+// reference's; only the storage (flat CSR) differs.
+#include "cloud.hpp"
+
+#include <algorithm>
+#include <cctype>
+#include <cerrno>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <limits>
+
+namespace kfb {
+
+namespace {
+
+constexpr double kSingularDetEps = 1e-12;  // pointcloud.hpp:50
+
+struct Naca4 {
+    double m, p, t;
+};
+
+// parse_naca, pointcloud.cpp:21-41
+Naca4 parse_digits(const std::string& d)
+{
+    bool ok = d.size() == 4;
+    for (char ch : d) ok = ok && std::isdigit(static_cast<unsigned char>(ch));
+    if (!ok)
+        throw IngestError(1, "invalid NACA code '" + d + "' (expected 4 digits)");
+    Naca4 s;
+    s.m = (d[0] - '0') / 100.0;
+    s.p = (d[1] - '0') / 10.0;
+    s.t = ((d[2] - '0') * 10 + (d[3] - '0')) / 100.0;
+    if (s.t <= 0.0) throw IngestError(1, "invalid NACA code '" + d + "' (zero thickness)");
+    if (s.m > 0.0 && s.p == 0.0)
+        throw IngestError(1, "invalid NACA code '" + d + "' (camber without camber position)");
+    return s;
+}
+
+// Closed-TE thickness polynomial and its slope, pointcloud.cpp:43-55
+double half_thickness(const Naca4& s, double x)
+{
+    return 5.0 * s.t *
+           (0.2969 * std::sqrt(x) - 0.1260 * x - 0.3516 * x * x + 0.2843 * x * x * x -
+            0.1036 * x * x * x * x);
+}
+double half_thickness_dx(const Naca4& s, double x)
+{
+    return 5.0 * s.t *
+           (0.14845 / std::sqrt(x) - 0.1260 - 0.7032 * x + 0.8529 * x * x -
+            0.4144 * x * x * x);
+}
+
+// Mean camber line, slope, curvature, pointcloud.cpp:57-76
+double camber_y(const Naca4& s, double x)
+{
+    if (s.m == 0.0) return 0.0;
+    if (x < s.p) return s.m / (s.p * s.p) * (2.0 * s.p * x - x * x);
+    return s.m / ((1.0 - s.p) * (1.0 - s.p)) * ((1.0 - 2.0 * s.p) + 2.0 * s.p * x - x * x);
+}
+double camber_dx(const Naca4& s, double x)
+{
+    if (s.m == 0.0) return 0.0;
+    if (x < s.p) return 2.0 * s.m / (s.p * s.p) * (s.p - x);
+    return 2.0 * s.m / ((1.0 - s.p) * (1.0 - s.p)) * (s.p - x);
+}
+double camber_dxx(const Naca4& s, double x)
+{
+    if (s.m == 0.0) return 0.0;
+    if (x < s.p) return -2.0 * s.m / (s.p * s.p);
+    return -2.0 * s.m / ((1.0 - s.p) * (1.0 - s.p));
+}
+
+struct WallSample {
+    double x, y, nx, ny;
+};
+
+// Surface point + outward normal at polar parameter theta, pointcloud.cpp:83-135
+WallSample surface_at(const Naca4& s, double theta)
+{
+    WallSample o;
+    const double xc = 0.5 * (1.0 + std::cos(theta));
+    const bool upper = theta < M_PI;
+    const double side = upper ? 1.0 : -1.0;
+    if (theta == 0.0) {
+        const double slope = camber_dx(s, 1.0);
+        const double len = std::hypot(1.0, slope);
+        o.x = 1.0;
+        o.y = camber_y(s, 1.0);
+        o.nx = 1.0 / len;
+        o.ny = slope / len;
+        return o;
+    }
+    if (std::fabs(theta - M_PI) < 1e-14) {
+        o.x = 0.0;
+        o.y = 0.0;
+        o.nx = -1.0;
+        o.ny = 0.0;
+        return o;
+    }
+    const double yt = half_thickness(s, xc);
+    const double yc = camber_y(s, xc);
+    const double dyc = camber_dx(s, xc);
+    const double delta = std::atan(dyc);
+    const double sd = std::sin(delta), cd = std::cos(delta);
+    o.x = xc - side * yt * sd;
+    o.y = yc + side * yt * cd;
+    const double dyt = half_thickness_dx(s, xc);
+    const double ddelta = camber_dxx(s, xc) / (1.0 + dyc * dyc);
+    const double tx = 1.0 - side * (dyt * sd + yt * cd * ddelta);
+    const double ty = dyc + side * (dyt * cd - yt * sd * ddelta);
+    const double dir = upper ? -1.0 : 1.0;
+    const double gx = dir * tx, gy = dir * ty;
+    const double len = std::hypot(gx, gy);
+    o.nx = gy / len;
+    o.ny = -gx / len;
+    return o;
+}
+
+// Bisection for the geometric stretch factor, pointcloud.cpp:152-168
+double stretch_factor(int levels, double target)
+{
+    auto first_gap = [&](double sg) { return (sg - 1.0) / (std::pow(sg, levels) - 1.0); };
+    double lo = 1.0 + 1e-9, hi = 3.0;
+    if (first_gap(hi) > target) return hi;
+    if (first_gap(lo) < target) return lo;
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (first_gap(mid) > target)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+struct Mom {
+    double xx = 0.0, yy = 0.0, xy = 0.0;
+};
+
+Mom moments_of(const Cloud& c, int p, const int* st, int m)
+{
+    Mom r;
+    for (int k = 0; k < m; ++k) {
+        const double dx = c.x[st[k]] - c.x[p];
+        const double dy = c.y[st[k]] - c.y[p];
+        r.xx += dx * dx;
+        r.yy += dy * dy;
+        r.xy += dx * dy;
+    }
+    return r;
+}
+
+// classify_moments, spatial.cpp:29-38
+int classify_moments(const Mom& m, int n)
+{
+    if (n == 0) return kEmpty;
+    if (m.xx == 0.0 && m.yy == 0.0) return kSingular;
+    if (m.yy == 0.0) return kLineX;
+    if (m.xx == 0.0) return kLineY;
+    const double det = m.xx * m.yy - m.xy * m.xy;
+    if (det < kSingularDetEps * m.xx * m.yy) return kSingular;
+    return kRegular;
+}
+
+// build_split_stencils' report predicate, pointcloud.cpp:264-277
+bool report_singular(const Cloud& c, int p, const int* st, int m)
+{
+    if (m == 0) return false;
+    const Mom r = moments_of(c, p, st, m);
+    if (r.xx == 0.0 || r.yy == 0.0) return false;
+    const double det = r.xx * r.yy - r.xy * r.xy;
+    return det < kSingularDetEps * r.xx * r.yy;
+}
+
+void split_stencils(Cloud& c)
+{
+    for (auto& s : c.split) {
+        s.off.assign(c.n + 1, 0);
+        s.idx.clear();
+        s.idx.reserve(c.nbr.idx.size() * 5 / 8 + 8);
+    }
+    c.empty_points.clear();
+    c.singular_points.clear();
+    for (int p = 0; p < c.n; ++p) {
+        for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1]; ++k) {
+            const int q = c.nbr.idx[k];
+            const double dx = c.x[q] - c.x[p];
+            const double dy = c.y[q] - c.y[p];
+            if (dx >= 0.0) c.split[kXpos].idx.push_back(q);
+            if (dx <= 0.0) c.split[kXneg].idx.push_back(q);
+            if (dy >= 0.0) c.split[kYpos].idx.push_back(q);
+            if (dy <= 0.0) c.split[kYneg].idx.push_back(q);
+        }
+        bool any_empty = false, any_singular = false;
+        for (auto& s : c.split) {
+            s.off[p + 1] = static_cast<int>(s.idx.size());
+            const int m = s.off[p + 1] - s.off[p];
+            any_empty = any_empty || m == 0;
+            any_singular = any_singular || report_singular(c, p, s.idx.data() + s.off[p], m);
+        }
+        any_singular = any_singular ||
+                       report_singular(c, p, c.nbr.idx.data() + c.nbr.off[p], c.nbr.degree(p));
+        if (any_empty) c.empty_points.push_back(p);
+        if (any_singular) c.singular_points.push_back(p);
+    }
+}
+
+// fill_split, spatial.cpp:40-76. axis_x: weight along x, else y.
+void split_weights(Cloud& c, int slot, bool axis_x, int p, bool& flagged)
+{
+    const Csr& s = c.split[slot];
+    const int b = s.off[p], m = s.off[p + 1] - b;
+    const int* st = s.idx.data() + b;
+    double* w = c.split_w[slot].data() + b;
+    for (int k = 0; k < m; ++k) w[k] = 0.0;
+    const Mom mo = moments_of(c, p, st, m);
+    const int cls = classify_moments(mo, m);
+    c.split_class[slot][p] = cls;
+    c.ls_one[slot][p] = 0.0;
+    if (cls == kEmpty) return;
+    if (cls == kSingular) {
+        flagged = true;
+        return;
+    }
+    if (cls == kLineX) {
+        if (!axis_x) return;
+        for (int k = 0; k < m; ++k) w[k] = (c.x[st[k]] - c.x[p]) / mo.xx;
+    } else if (cls == kLineY) {
+        if (axis_x) return;
+        for (int k = 0; k < m; ++k) w[k] = (c.y[st[k]] - c.y[p]) / mo.yy;
+    } else {
+        const double den = mo.xx * mo.yy - mo.xy * mo.xy;
+        for (int k = 0; k < m; ++k) {
+            const double dx = c.x[st[k]] - c.x[p];
+            const double dy = c.y[st[k]] - c.y[p];
+            w[k] = axis_x ? (mo.yy * dx - mo.xy * dy) / den : (mo.xx * dy - mo.xy * dx) / den;
+        }
+    }
+    double sum = 0.0;
+    for (int k = 0; k < m; ++k) sum += w[k];
+    c.ls_one[slot][p] = sum;
+}
+
+void ls_operators(Cloud& c)
+{
+    const size_t nnz = c.nbr.idx.size();
+    c.wx.assign(nnz, 0.0);
+    c.wy.assign(nnz, 0.0);
+    c.full_class.assign(c.n, kEmpty);
+    for (int s = 0; s < 4; ++s) {
+        c.split_w[s].assign(c.split[s].idx.size(), 0.0);
+        c.ls_one[s].assign(c.n, 0.0);
+        c.split_class[s].assign(c.n, kEmpty);
+    }
+    c.flagged.clear();
+    for (int p = 0; p < c.n; ++p) {
+        bool flagged = false;
+        const int b = c.nbr.off[p], m = c.nbr.degree(p);
+        const int* st = c.nbr.idx.data() + b;
+        const Mom mo = moments_of(c, p, st, m);
+        const int cls = classify_moments(mo, m);
+        c.full_class[p] = cls;
+        if (cls == kRegular) {
+            const double den = mo.xx * mo.yy - mo.xy * mo.xy;
+            for (int k = 0; k < m; ++k) {
+                const double dx = c.x[st[k]] - c.x[p];
+                const double dy = c.y[st[k]] - c.y[p];
+                c.wx[b + k] = (mo.yy * dx - mo.xy * dy) / den;
+                c.wy[b + k] = (mo.xx * dy - mo.xy * dx) / den;
+            }
+        } else if (cls == kLineX) {
+            for (int k = 0; k < m; ++k) c.wx[b + k] = (c.x[st[k]] - c.x[p]) / mo.xx;
+        } else if (cls == kLineY) {
+            for (int k = 0; k < m; ++k) c.wy[b + k] = (c.y[st[k]] - c.y[p]) / mo.yy;
+        } else if (cls == kSingular) {
+            flagged = true;
+        }
+        split_weights(c, kXpos, true, p, flagged);
+        split_weights(c, kXneg, true, p, flagged);
+        split_weights(c, kYpos, false, p, flagged);
+        split_weights(c, kYneg, false, p, flagged);
+        if (flagged) c.flagged.push_back(p);
+    }
+}
+
+// Greedy colouring over the symmetrised graph, coloring.cpp:7-52.
+void greedy_colors(Cloud& c)
+{
+    const int n = c.n;
+    std::vector<int> deg(n + 1, 0);
+    for (int i = 0; i < n; ++i)
+        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k) {
+            ++deg[i];
+            ++deg[c.nbr.idx[k]];
+        }
+    std::vector<long> aoff(n + 1, 0);
+    for (int i = 0; i < n; ++i) aoff[i + 1] = aoff[i] + deg[i];
+    std::vector<int> adj(aoff[n]);
+    std::vector<long> pos(aoff.begin(), aoff.end() - 1);
+    for (int i = 0; i < n; ++i)
+        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k) {
+            const int q = c.nbr.idx[k];
+            adj[pos[i]++] = q;
+            adj[pos[q]++] = i;
+        }
+    std::vector<int> len(n);
+    for (int i = 0; i < n; ++i) {
+        int* a = adj.data() + aoff[i];
+        const int m = static_cast<int>(aoff[i + 1] - aoff[i]);
+        std::sort(a, a + m);
+        len[i] = static_cast<int>(std::unique(a, a + m) - a);
+    }
+    c.color.assign(n, 0);
+    if (n > 0) c.color[0] = 1;
+    std::vector<char> seen;
+    for (int i = 0; i < n; ++i) {
+        for (int t = 0; t < len[i]; ++t) {
+            const int p = adj[aoff[i] + t];
+            if (c.color[p] != 0) continue;
+            seen.assign(static_cast<size_t>(len[p]) + 2, 0);
+            for (int u = 0; u < len[p]; ++u) {
+                const int cq = c.color[adj[aoff[p] + u]];
+                if (cq > 0 && cq < static_cast<int>(seen.size())) seen[cq] = 1;
+            }
+            int k = 1;
+            while (seen[k]) ++k;
+            c.color[p] = k;
+        }
+    }
+    for (int i = 0; i < n; ++i)
+        if (c.color[i] == 0) c.color[i] = 1;
+    c.n_colors = n > 0 ? *std::max_element(c.color.begin(), c.color.end()) : 0;
+}
+
+// Minimal istream-like scanner over one line (pointcloud.cpp:310-356 reads
+// each record with operator>>).
+struct LineScanner {
+    const char* s;
+    bool get_long(long& v)
+    {
+        char* end = nullptr;
+        errno = 0;
+        const long r = std::strtol(s, &end, 10);
+        if (end == s || errno == ERANGE) return false;
+        v = r;
+        s = end;
+        return true;
+    }
+    bool get_int(int& v)
+    {
+        long t;
+        if (!get_long(t) || t < std::numeric_limits<int>::min() ||
+            t > std::numeric_limits<int>::max())
+            return false;
+        v = static_cast<int>(t);
+        return true;
+    }
+    bool get_double(double& v)
+    {
+        char* end = nullptr;
+        const double r = std::strtod(s, &end);
+        if (end == s) return false;
+        v = r;
+        s = end;
+        return true;
+    }
+};
+
+}  // namespace
+
+void finalize(Cloud& c)
+{
+    c.wall_ids.clear();
+    c.interior_ids.clear();
+    c.outer_ids.clear();
+    for (int i = 0; i < c.n; ++i) {
+        if (c.kind[i] == kWall) c.wall_ids.push_back(i);
+        if (c.kind[i] == kInterior) c.interior_ids.push_back(i);
+        if (c.kind[i] == kOuter) c.outer_ids.push_back(i);
+    }
+    split_stencils(c);
+    ls_operators(c);
+    greedy_colors(c);
+}
+
+Cloud generate_naca_ogrid(const std::string& digits, int n_wall, int n_radial,
+                          double far_field_radius)
+{
+    const Naca4 shape = parse_digits(digits);
+    if (n_wall < 32 || n_radial < 8 || far_field_radius < 10.0)
+        throw IngestError(1,
+                          "degenerate O-grid parameters (need n_wall >= 32, n_radial >= 8, "
+                          "far_field_radius >= 10)");
+    const double cx = 0.5, cy = 0.0;
+    const long N = static_cast<long>(n_wall) * n_radial;
+    if (N > std::numeric_limits<int>::max() / 8)
+        throw IngestError(1, "O-grid too large for 32-bit indexing");
+    Cloud c;
+    c.n = static_cast<int>(N);
+    c.x.resize(N);
+    c.y.resize(N);
+    c.nx.assign(N, 0.0);
+    c.ny.assign(N, 0.0);
+    c.kind.assign(N, kInterior);
+
+    std::vector<WallSample> wall(n_wall);
+    for (int i = 0; i < n_wall; ++i) wall[i] = surface_at(shape, 2.0 * M_PI * i / n_wall);
+    double perimeter = 0.0;
+    for (int i = 0; i < n_wall; ++i) {
+        const WallSample& a = wall[i];
+        const WallSample& b = wall[(i + 1) % n_wall];
+        perimeter += std::hypot(b.x - a.x, b.y - a.y);
+    }
+    const double first_layer = perimeter / n_wall;
+    const double mean_ray = far_field_radius - 0.5;
+    const double sigma = stretch_factor(n_radial - 1, first_layer / mean_ray);
+    std::vector<double> frac(n_radial);
+    for (int j = 0; j < n_radial; ++j)
+        frac[j] = (std::pow(sigma, j) - 1.0) / (std::pow(sigma, n_radial - 1) - 1.0);
+
+    for (int i = 0; i < n_wall; ++i) {
+        const WallSample& s = wall[i];
+        const double phi = std::atan2(s.y - cy, s.x - cx);
+        const double fx = cx + far_field_radius * std::cos(phi);
+        const double fy = cy + far_field_radius * std::sin(phi);
+        for (int j = 0; j < n_radial; ++j) {
+            const long id = static_cast<long>(j) * n_wall + i;
+            c.x[id] = s.x + frac[j] * (fx - s.x);
+            c.y[id] = s.y + frac[j] * (fy - s.y);
+            if (j == 0) {
+                c.kind[id] = kWall;
+                c.nx[id] = s.nx;
+                c.ny[id] = s.ny;
+            } else if (j == n_radial - 1) {
+                c.kind[id] = kOuter;
+                c.nx[id] = std::cos(phi);
+                c.ny[id] = std::sin(phi);
+            }
+        }
+    }
+
+    // Eight-neighbourhood, wrapped in i and clamped in j (pointcloud.cpp:237-250).
+    c.nbr.off.assign(N + 1, 0);
+    c.nbr.idx.reserve(N * 8);
+    for (int j = 0; j < n_radial; ++j) {
+        for (int i = 0; i < n_wall; ++i) {
+            const long id = static_cast<long>(j) * n_wall + i;
+            for (int dj = -1; dj <= 1; ++dj) {
+                const int jj = j + dj;
+                if (jj < 0 || jj >= n_radial) continue;
+                for (int di = -1; di <= 1; ++di) {
+                    if (di == 0 && dj == 0) continue;
+                    const int ii = (i + di + n_wall) % n_wall;
+                    c.nbr.idx.push_back(jj * n_wall + ii);
+                }
+            }
+            c.nbr.off[id + 1] = static_cast<int>(c.nbr.idx.size());
+        }
+    }
+    finalize(c);
+    return c;
+}
+
+Cloud cloud_from_arrays(int n, const double* x, const double* y, const int* kind,
+                        const double* nx, const double* ny, const int* off, const int* idx)
+{
+    if (n < 0) throw IngestError(1, "negative point count");
+    Cloud c;
+    c.n = n;
+    c.x.assign(x, x + n);
+    c.y.assign(y, y + n);
+    c.nx.assign(nx, nx + n);
+    c.ny.assign(ny, ny + n);
+    c.kind.assign(kind, kind + n);
+    c.nbr.off.assign(off, off + n + 1);
+    if (off[0] != 0) throw IngestError(1, "neighbour offsets must start at 0");
+    for (int p = 0; p < n; ++p) {
+        if (off[p + 1] < off[p]) throw IngestError(1, "neighbour offsets must be nondecreasing");
+        if (kind[p] < 0 || kind[p] > 2) throw IngestError(1, "bad point kind at point " + std::to_string(p));
+    }
+    c.nbr.idx.assign(idx, idx + off[n]);
+    for (int q : c.nbr.idx)
+        if (q < 0 || q >= n) throw IngestError(1, "neighbour id out of range");
+    finalize(c);
+    return c;
+}
+
+Cloud load_cloud(const std::string& path)
+{
+    std::ifstream in(path);
+    if (!in) throw IngestError(2, "cannot open cloud file: " + path);
+    Cloud c;
+    long expected = -1;
+    int lineno = 0;
+    std::string line;
+    std::vector<int> nb;
+    auto fail = [&](const std::string& why) {
+        throw IngestError(2, path + ":" + std::to_string(lineno) + ": parse error: " + why);
+    };
+    c.nbr.off.push_back(0);
+    while (std::getline(in, line)) {
+        ++lineno;
+        const size_t first = line.find_first_not_of(" \t\r");
+        if (first == std::string::npos || line[first] == '#') continue;
+        LineScanner sc{line.c_str()};
+        if (expected < 0) {
+            if (!sc.get_long(expected) || expected <= 0) fail("bad point count header");
+            c.x.reserve(expected);
+            continue;
+        }
+        long pid;
+        double px, py;
+        int kd, nn;
+        if (!(sc.get_long(pid) && sc.get_double(px) && sc.get_double(py) && sc.get_int(kd) &&
+              sc.get_int(nn)))
+            fail("bad point record");
+        if (pid != static_cast<long>(c.x.size()) + 1)
+            fail("point index " + std::to_string(pid) + " out of order");
+        if (kd < 0 || kd > 2) fail("bad point kind " + std::to_string(kd));
+        if (nn < 0) fail("negative neighbour count");
+        nb.assign(nn, 0);
+        for (int k = 0; k < nn; ++k) {
+            long v;
+            if (!sc.get_long(v)) fail("missing neighbour id");
+            nb[k] = static_cast<int>(v - 1);
+        }
+        double vx = 0.0, vy = 0.0;
+        if (kd == kWall || kd == kOuter) {
+            if (!(sc.get_double(vx) && sc.get_double(vy))) fail("missing normal for boundary point");
+        }
+        c.x.push_back(px);
+        c.y.push_back(py);
+        c.kind.push_back(kd);
+        c.nx.push_back(vx);
+        c.ny.push_back(vy);
+        c.nbr.idx.insert(c.nbr.idx.end(), nb.begin(), nb.end());
+        c.nbr.off.push_back(static_cast<int>(c.nbr.idx.size()));
+    }
+    if (expected < 0) throw IngestError(2, path + ": empty cloud file");
+    if (static_cast<long>(c.x.size()) != expected)
+        throw IngestError(2, path + ": expected " + std::to_string(expected) + " points, found " +
+                                 std::to_string(c.x.size()));
+    c.n = static_cast<int>(c.x.size());
+    for (int i = 0; i < c.n; ++i) {
+        if (c.nbr.degree(i) < 3)
+            throw IngestError(2, path + ": point " + std::to_string(i + 1) +
+                                     " has fewer than 3 neighbours");
+        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k) {
+            const int q = c.nbr.idx[k];
+            if (q < 0 || q >= c.n)
+                throw IngestError(2, path + ": point " + std::to_string(i + 1) +
+                                         " has out-of-range neighbour " + std::to_string(q + 1));
+            if (q == i)
+                throw IngestError(2, path + ": point " + std::to_string(i + 1) +
+                                         " lists itself as neighbour");
+        }
+        if (c.kind[i] != kInterior) {
+            const double len = std::hypot(c.nx[i], c.ny[i]);
+            if (std::fabs(len - 1.0) > 1e-6)
+                throw IngestError(2, path + ": point " + std::to_string(i + 1) +
+                                         " has a non-unit normal");
+        }
+    }
+    finalize(c);
+    return c;
+}
+
+void save_cloud(const Cloud& c, const std::string& path)
+{
+    std::FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw IngestError(2, "cannot write cloud file: " + path);
+    std::fprintf(f, "%d\n", c.n);
+    for (int i = 0; i < c.n; ++i) {
+        std::fprintf(f, "%d %.17g %.17g %d %d", i + 1, c.x[i], c.y[i], c.kind[i], c.nbr.degree(i));
+        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k) std::fprintf(f, " %d", c.nbr.idx[k] + 1);
+        if (c.kind[i] != kInterior) std::fprintf(f, " %.17g %.17g", c.nx[i], c.ny[i]);
+        std::fputc('\n', f);
+    }
+    std::fclose(f);
+}
+
+}  // namespace kfb

@@ -1,0 +1,75 @@
+"""The C-ABI library (CPU only): it loads, exports every symbol include/kf.h
+declares, and the device entry points fail loudly (no CPU fallback) when no
+GPU is present.
+"""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2406_07441_b200 as kf
+from paper_2406_07441_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "kf.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(kf_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_declares_what_binding_expects():
+    assert sorted(_lib.EXPORTED) == declared_symbols()
+
+
+def test_library_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(l.split()[-1] for l in out.splitlines() if l.strip())
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_version_and_defaults():
+    assert "sm_100a" in kf.version()
+    cfg = _lib.Config()
+    _lib.lib.kf_config_default(C.byref(cfg))
+    # SolverConfig defaults, driver.hpp:37-52
+    assert (cfg.variant, cfg.cfl, cfg.n_iterations, cfg.n_inner, cfg.mach_inf) == (0, 0.2, 100, 3, 0.63)
+    assert cfg.divergence_factor == 1e6 and cfg.bc_mode == 0
+
+
+def test_preconditions_raise_like_reference():
+    c = kf.generate_naca_ogrid("0012", 32, 8, 10.0)
+    with pytest.raises(kf.ConfigError, match="cfl must be positive"):
+        kf.Solver(c, kf.SolverConfig(cfl=0.0))
+    with pytest.raises(kf.ConfigError, match="n_iterations"):
+        kf.Solver(c, kf.SolverConfig(n_iterations=0))
+
+
+def test_no_gpu_fails_loudly(has_gpu):
+    if has_gpu:
+        pytest.skip("GPU present")
+    c = kf.generate_naca_ogrid("0012", 32, 8, 10.0)
+    with pytest.raises(kf.CudaError, match="no CUDA device"):
+        kf.Solver(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD))
+    with pytest.raises(kf.CudaError):
+        kf.split_flux(np.array([[1.0, 0.1, 0.0, 2.5]]), 0, 0)
+
+
+def test_singular_interior_stencil_refused():
+    # driver.cpp:198-201: an interior point with a singular LS stencil aborts setup
+    from util import hand_cloud
+    c = kf.PointCloud.from_arrays(*hand_cloud([(0, 0), (1, 1), (2, 2), (-1, -1)],
+                                              [[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]]))
+    with pytest.raises(kf.KinfreeError, match="singular least-squares stencil"):
+        kf.Solver(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD))
