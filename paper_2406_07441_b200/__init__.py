@@ -30,6 +30,7 @@ from .api import (  # noqa: F401
     jvp_full,
     jvp_split,
     load_cloud,
+    measure_fp64_peak,
     run_fixed_point,
     save_cloud,
     set_colors,

@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -141,6 +142,9 @@ struct Solver::Impl {
     long long total_counters[5] = {0, 0, 0, 0, 0};
     int forces_err = 0;
     int res_blocks = 0;
+    bool flux16 = true;
+    bool grad8 = true;
+    int flux_minb = 2;
     int launches = 0;
     int launches_bench = 0;
     std::vector<DevRecord> rec_h;
@@ -151,6 +155,21 @@ struct Solver::Impl {
     ~Impl();
     void pack(const Cloud& c);
     void enqueue_iteration(int cur_buf, double cfl_override, bool with_q);
+    void launch_grad(bool first, int src, int dst)
+    {
+        if (grad8) {
+            const int b = blocks_for(static_cast<long>(n_pad) * 8, kGradThreads);
+            if (first)
+                k_grad8<true><<<b, kGradThreads, 0, s>>>(D, src, dst);
+            else
+                k_grad8<false><<<b, kGradThreads, 0, s>>>(D, src, dst);
+        } else {
+            if (first)
+                k_grad<true><<<blocks_for(n_pad, kThreads), kThreads, 0, s>>>(D, src, dst);
+            else
+                k_grad<false><<<blocks_for(n_pad, kThreads), kThreads, 0, s>>>(D, src, dst);
+        }
+    }
     void build_graphs();
     void upload_ref4(double4* dst, const double* host);
     void download_ref4(double* host, const double4* src);
@@ -422,7 +441,18 @@ void Solver::Impl::pack(const Cloud& c)
     D.dt_out = nullptr;
     D.S_out = nullptr;
     D.cp = dalloc<double>(std::max(W, 1), owned);
-    res_blocks = blocks_for(n_pad, kThreads);
+    {
+        // A/B switch: "point" = one thread per point, "lanes3" = 16 lanes with
+        // a 3-blocks/SM register cap, default "lanes2"
+        const char* env = std::getenv("KF_FLUX_KERNEL");
+        const std::string v = env ? env : "lanes2";
+        flux16 = v != "point";
+        flux_minb = v == "lanes3" ? 3 : 2;
+        const char* g = std::getenv("KF_GRAD_KERNEL");  // "point" = one thread/point
+        grad8 = !(g && std::string(g) == "point");
+    }
+    res_blocks = flux16 ? blocks_for(static_cast<long>(n_pad) * kResLanes, kResThreads)
+                        : blocks_for(n_pad, kThreads);
     D.res_part = dalloc<double>(res_blocks, owned);
     D.cnt_part = dalloc<long long>(res_blocks, owned);
     D.fo_part = dalloc<int>(res_blocks, owned);
@@ -431,6 +461,7 @@ void Solver::Impl::pack(const Cloud& c)
     D.n_fb_parts = 1;
     D.status = dalloc<unsigned long long>(1, owned);
     D.iter = dalloc<int>(1, owned);
+    D.nrec = dalloc<int>(1, owned);
     D.res0 = dalloc<double>(1, owned);
     D.diverged = dalloc<int>(1, owned);
     D.tstamp = dalloc<unsigned long long>(1, owned);
@@ -502,15 +533,20 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
         k_q_from_u<<<blocks_for(n_pad, 256), 256, 0, s>>>(D, cb, 0);
         mark("q_from_u");
     }
-    k_grad<true><<<blocks_for(n_pad, T), T, 0, s>>>(D, 0, 0);
+    launch_grad(true, 0, 0);
     mark("grad_pass1");
     int slot = 0;
     for (int pass = 2; pass <= cfg.n_inner; ++pass) {
-        k_grad<false><<<blocks_for(n_pad, T), T, 0, s>>>(D, slot, slot ^ 1);
+        launch_grad(false, slot, slot ^ 1);
         slot ^= 1;
         mark("grad_passk");
     }
-    k_residual<<<res_blocks, T, 0, s>>>(D, slot, 0);
+    if (flux16 && flux_minb == 3)
+        k_residual16<3><<<res_blocks, kResThreads, 0, s>>>(D, slot, 0);
+    else if (flux16)
+        k_residual16<2><<<res_blocks, kResThreads, 0, s>>>(D, slot, 0);
+    else
+        k_residual<<<res_blocks, T, 0, s>>>(D, slot, 0);
     mark("flux_residual");
     if (D.implicit) {
         for (int c = 0; c < C; ++c) {
@@ -640,6 +676,7 @@ void Solver::reset()
     const double m1 = -1.0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.diverged, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.fb_part, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.res0, &m1, sizeof m1, cudaMemcpyHostToDevice, I.s), "H2D");
@@ -663,6 +700,7 @@ void Solver::set_state(const double* U, const double* dU_prev)
     const int zero = 0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     k_q_from_u<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, 0, 1);
     k_stamp<<<1, 1, 0, I.s>>>(I.D);
     ck(cudaStreamSynchronize(I.s), "set_state");
@@ -725,7 +763,7 @@ void Solver::bench_mode(int mode)
     // snapshot the current state (I.cur) and the iteration counter
     ck(cudaMemcpyAsync(I.Usnap, I.D.U[I.cur], sizeof(double4) * I.n_pad, cudaMemcpyDeviceToDevice, I.s), "D2D");
     ck(cudaMemcpyAsync(I.dUsnap, I.D.dU, sizeof(double4) * I.n_pad, cudaMemcpyDeviceToDevice, I.s), "D2D");
-    ck(cudaMemcpyAsync(I.h_iter, I.D.iter, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
+    ck(cudaMemcpyAsync(I.h_iter, I.D.nrec, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
     ck(cudaStreamSynchronize(I.s), "sync");
     I.snap_iter = std::min(*I.h_iter, I.D.rec_capacity - 1);
     I.bench = 1;
@@ -745,7 +783,7 @@ int Solver::sync_records(kf_iter_record* records, int capacity, int* n_done, std
 {
     Impl& I = *impl_;
     ck(cudaMemcpyAsync(I.h_status, I.D.status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, I.s), "D2H");
-    ck(cudaMemcpyAsync(I.h_iter, I.D.iter, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
+    ck(cudaMemcpyAsync(I.h_iter, I.D.nrec, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
     ck(cudaStreamSynchronize(I.s), "sync");
     int nd = std::min(*I.h_iter, I.D.rec_capacity);
     if (n_done) *n_done = nd;
@@ -853,6 +891,7 @@ int Solver::step_host(const double* U_in, const double* dU_in, double* U_out, do
     const int zero = 0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     if (I.cfg.use_graph && I.bench_graph)
         ck(cudaGraphLaunch(I.bench_graph, I.s), "graph launch");
     else
@@ -882,6 +921,7 @@ int Solver::stage_q(const double* U, double* q, std::string& reason, int& point)
     const int zero = 0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     k_q_from_u<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, 0, 1);
     I.download_ref4(q, I.D.q);
     d2h(I.h_status, I.D.status, 1, I.s);
@@ -901,11 +941,12 @@ int Solver::stage_grads(const double* q, double* qx, double* qy)
     const int zero = 0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     I.upload_ref4(I.D.q, q);
-    k_grad<true><<<blocks_for(I.n_pad, kThreads), kThreads, 0, I.s>>>(I.D, 0, 0);
+    I.launch_grad(true, 0, 0);
     int slot = 0;
     for (int pass = 2; pass <= I.cfg.n_inner; ++pass) {
-        k_grad<false><<<blocks_for(I.n_pad, kThreads), kThreads, 0, I.s>>>(I.D, slot, slot ^ 1);
+        I.launch_grad(false, slot, slot ^ 1);
         slot ^= 1;
     }
     I.download_ref4(qx, I.D.qx[slot]);
@@ -923,12 +964,16 @@ int Solver::stage_residual(const double* q, const double* qx, const double* qy, 
     const int zero = 0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     I.upload_ref4(I.D.q, q);
     ck(cudaStreamSynchronize(I.s), "sync");
     I.upload_ref4(I.D.qx[0], qx);
     ck(cudaStreamSynchronize(I.s), "sync");
     I.upload_ref4(I.D.qy[0], qy);
-    k_residual<<<I.res_blocks, kThreads, 0, I.s>>>(I.D, 0, 0);
+    if (I.flux16)
+        k_residual16<2><<<I.res_blocks, kResThreads, 0, I.s>>>(I.D, 0, 0);
+    else
+        k_residual<<<I.res_blocks, kThreads, 0, I.s>>>(I.D, 0, 0);
     I.download_ref4(R, I.D.R);
     ck(cudaStreamSynchronize(I.s), "sync");
     if (demoted) {
@@ -955,6 +1000,7 @@ int Solver::stage_lusgs(const double* U, const double* R, const double* dU_prev,
     const int zero = 0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     I.upload_ref4(I.D.U[0], U);
     ck(cudaStreamSynchronize(I.s), "sync");
     I.upload_ref4(I.D.R, R);
@@ -1009,6 +1055,7 @@ int Solver::stage_update(const double* U, const double* dU, double* U_out, std::
     const int zero = 0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     I.upload_ref4(I.D.U[0], U);
     ck(cudaStreamSynchronize(I.s), "sync");
     I.upload_ref4(I.D.dU, dU);
@@ -1032,6 +1079,7 @@ int Solver::stage_forces(const double* U, double* cl, double* cd, std::string& r
     const int zero = 0;
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemsetAsync(I.D.res_part, 0, sizeof(double) * I.res_blocks, I.s), "memset");
     ck(cudaMemsetAsync(I.D.cnt_part, 0, sizeof(long long) * I.res_blocks, I.s), "memset");
     ck(cudaMemsetAsync(I.D.fo_part, 0, sizeof(int) * I.res_blocks, I.s), "memset");
