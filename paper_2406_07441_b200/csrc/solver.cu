@@ -96,6 +96,22 @@ __global__ void k_to_ref_u8(int* dst, const unsigned char* src, const int* orig,
     const int o = orig[p];
     if (o >= 0) dst[o] = src[p];
 }
+__device__ __forceinline__ double4& rec_field(PtRec& r, int f) { return f == 0 ? r.q : f == 1 ? r.qx : r.qy; }
+__global__ void k_ref_to_rec(PtRec* dst, int field, const double4* src, const int* orig, int n_pad)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pad) return;
+    const int o = orig[p];
+    rec_field(dst[p], field) = o >= 0 ? src[o] : make_double4(0, 0, 0, 0);
+}
+__global__ void k_rec_to_ref(double4* dst, const PtRec* src, int field, const int* orig, int n_pad)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pad) return;
+    const int o = orig[p];
+    PtRec r = src[p];
+    if (o >= 0) dst[o] = rec_field(r, field);
+}
 __global__ void k_cp(Dev D, int buf)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -142,9 +158,7 @@ struct Solver::Impl {
     long long total_counters[5] = {0, 0, 0, 0, 0};
     int forces_err = 0;
     int res_blocks = 0;
-    bool flux16 = true;
-    bool grad8 = true;
-    int flux_minb = 2;
+    int flux_variant = 0;  // residual kernel: 0 exact/3 blocks, 1 exact/4, 2 fast/3, 3 fast/4
     int launches = 0;
     int launches_bench = 0;
     std::vector<DevRecord> rec_h;
@@ -157,21 +171,24 @@ struct Solver::Impl {
     void enqueue_iteration(int cur_buf, double cfl_override, bool with_q);
     void launch_grad(bool first, int src, int dst)
     {
-        if (grad8) {
-            const int b = blocks_for(static_cast<long>(n_pad) * 8, kGradThreads);
-            if (first)
-                k_grad8<true><<<b, kGradThreads, 0, s>>>(D, src, dst);
-            else
-                k_grad8<false><<<b, kGradThreads, 0, s>>>(D, src, dst);
-        } else {
-            if (first)
-                k_grad<true><<<blocks_for(n_pad, kThreads), kThreads, 0, s>>>(D, src, dst);
-            else
-                k_grad<false><<<blocks_for(n_pad, kThreads), kThreads, 0, s>>>(D, src, dst);
+        if (first)
+            k_grad<true><<<blocks_for(n_pad, kThreads), kThreads, 0, s>>>(D, src, dst);
+        else
+            k_grad<false><<<blocks_for(n_pad, kThreads), kThreads, 0, s>>>(D, src, dst);
+    }
+    void launch_residual(int gslot)
+    {
+        switch (flux_variant) {
+            case 1: k_residual<4, false><<<res_blocks, kThreads, 0, s>>>(D, gslot, 0); break;
+            case 2: k_residual<3, true><<<res_blocks, kThreads, 0, s>>>(D, gslot, 0); break;
+            case 3: k_residual<4, true><<<res_blocks, kThreads, 0, s>>>(D, gslot, 0); break;
+            default: k_residual<3, false><<<res_blocks, kThreads, 0, s>>>(D, gslot, 0); break;
         }
     }
     void build_graphs();
     void upload_ref4(double4* dst, const double* host);
+    void upload_field(PtRec* dst, int field, const double* host);
+    void download_field(double* host, const PtRec* src, int field);
     void download_ref4(double* host, const double4* src);
     std::string message(unsigned long long key, int& point, int& iteration) const;
     void fill_record(kf_iter_record& out, const DevRecord& r, bool accumulate);
@@ -260,8 +277,12 @@ void Solver::Impl::pack(const Cloud& c)
         slice_off[sl + 1] = slice_off[sl] + 32 * w;
     }
     const size_t n_e = static_cast<size_t>(slice_off[n_slices]);
-    std::vector<int> e_nbr(n_e, -1);
-    std::vector<double2> e_dxy(n_e, make_double2(0, 0)), e_wxy(n_e, make_double2(0, 0));
+    // slots past a point's degree refer to the point itself with zero weights
+    std::vector<int> e_nbr(n_e, 0);
+    for (int pn = 0; pn < n_pad; ++pn)
+        for (size_t e = slice_off[pn >> 5] + (pn & 31); e < static_cast<size_t>(slice_off[(pn >> 5) + 1]); e += 32)
+            e_nbr[e] = pn;
+    std::vector<double2> e_wxy(n_e, make_double2(0, 0));
     std::vector<double4> e_w4(n_e, make_double4(0, 0, 0, 0));
     nnz_w = 0;
     for (int pn = 0; pn < n_pad; ++pn) {
@@ -295,7 +316,6 @@ void Solver::Impl::pack(const Cloud& c)
             const int kk = k - c.nbr.off[o];
             const size_t e = static_cast<size_t>(slice_off[pn >> 5]) + 32 * kk + (pn & 31);
             e_nbr[e] = inv[i];
-            e_dxy[e] = make_double2(dx, dy);
             e_wxy[e] = make_double2(c.wx[k], c.wy[k]);
             // the split-list entries that this full-stencil entry became
             // (pointcloud.cpp:281-289 appends in nbr order)
@@ -316,7 +336,6 @@ void Solver::Impl::pack(const Cloud& c)
     }
     // ---- wall loop geometry for compute_forces (driver.cpp:127-167)
     const int W = static_cast<int>(c.wall_ids.size());
-    std::vector<int> wall_new(std::max(W, 1), 0);
     std::vector<double> oty(std::max(W, 1), 0.0), otx(std::max(W, 1), 0.0);
     forces_err = 0;
     if (W < 3) {
@@ -338,7 +357,6 @@ void Solver::Impl::pack(const Cloud& c)
             const double ty = c.y[b] - c.y[a];
             oty[k] = orient * ty;
             otx[k] = orient * (-tx);
-            wall_new[k] = inv[a];
             wslot[inv[a]] = k;
         }
     }
@@ -413,9 +431,6 @@ void Solver::Impl::pack(const Cloud& c)
     int* d_enbr = dalloc<int>(n_e, owned);
     up(d_enbr, e_nbr);
     D.e_nbr = d_enbr;
-    double2* d_edxy = dalloc<double2>(n_e, owned);
-    up(d_edxy, e_dxy);
-    D.e_dxy = d_edxy;
     double2* d_ewxy = dalloc<double2>(n_e, owned);
     up(d_ewxy, e_wxy);
     D.e_wxy = d_ewxy;
@@ -425,14 +440,22 @@ void Solver::Impl::pack(const Cloud& c)
 
     for (int b = 0; b < 2; ++b) {
         D.U[b] = dalloc<double4>(n_pad, owned);
-        D.qx[b] = dalloc<double4>(n_pad, owned);
-        D.qy[b] = dalloc<double4>(n_pad, owned);
+        D.P[b] = dalloc<PtRec>(n_pad, owned);
     }
-    D.q = dalloc<double4>(n_pad, owned);
+    {
+        std::vector<PtRec> rec(n_pad);
+        for (int pn = 0; pn < n_pad; ++pn) {
+            rec[pn] = PtRec{};
+            const int o = perm[pn];
+            rec[pn].xy = o >= 0 ? make_double2(c.x[o], c.y[o]) : make_double2(0, 0);
+        }
+        up(D.P[0], rec);
+        up(D.P[1], rec);
+    }
     D.R = dalloc<double4>(n_pad, owned);
     D.dUs = dalloc<double4>(n_pad, owned);
     D.dU = dalloc<double4>(n_pad, owned);
-    D.J = dalloc<double4>(4 * static_cast<size_t>(n_pad), owned);
+    D.J = dalloc<JRec>(n_pad, owned);
     D.jbad = dalloc<unsigned char>(n_pad, owned);
     D.diag = dalloc<double>(n_pad, owned);
     D.demoted = dalloc<unsigned char>(n_pad, owned);
@@ -442,23 +465,17 @@ void Solver::Impl::pack(const Cloud& c)
     D.S_out = nullptr;
     D.cp = dalloc<double>(std::max(W, 1), owned);
     {
-        // A/B switch: "point" = one thread per point, "lanes3" = 16 lanes with
-        // a 3-blocks/SM register cap, default "lanes2"
+        // A/B switch for the residual kernel (register cap x arithmetic)
         const char* env = std::getenv("KF_FLUX_KERNEL");
-        const std::string v = env ? env : "lanes2";
-        flux16 = v != "point";
-        flux_minb = v == "lanes3" ? 3 : 2;
-        const char* g = std::getenv("KF_GRAD_KERNEL");  // "point" = one thread/point
-        grad8 = !(g && std::string(g) == "point");
+        const std::string v = env ? env : "m3";
+        flux_variant = v == "m4" ? 1 : v == "m3fast" ? 2 : v == "m4fast" ? 3 : 0;
     }
-    res_blocks = flux16 ? blocks_for(static_cast<long>(n_pad) * kResLanes, kResThreads)
-                        : blocks_for(n_pad, kThreads);
+    res_blocks = blocks_for(n_pad, kThreads);
     D.res_part = dalloc<double>(res_blocks, owned);
     D.cnt_part = dalloc<long long>(res_blocks, owned);
     D.fo_part = dalloc<int>(res_blocks, owned);
     D.fb_part = dalloc<int>(1, owned);
     D.n_res_blocks = res_blocks;
-    D.n_fb_parts = 1;
     D.status = dalloc<unsigned long long>(1, owned);
     D.iter = dalloc<int>(1, owned);
     D.nrec = dalloc<int>(1, owned);
@@ -494,9 +511,6 @@ void Solver::Impl::pack(const Cloud& c)
     D.div_factor = cfg.divergence_factor;
     D.conv_factor = cfg.convergence_decades > 0.0 ? std::pow(10.0, -cfg.convergence_decades) : -1.0;
     D.W = W;
-    int* d_wall = dalloc<int>(wall_new.size(), owned);
-    up(d_wall, wall_new);
-    D.wall_new = d_wall;
     double* d_oty = dalloc<double>(oty.size(), owned);
     up(d_oty, oty);
     D.oty = d_oty;
@@ -541,12 +555,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
         slot ^= 1;
         mark("grad_passk");
     }
-    if (flux16 && flux_minb == 3)
-        k_residual16<3><<<res_blocks, kResThreads, 0, s>>>(D, slot, 0);
-    else if (flux16)
-        k_residual16<2><<<res_blocks, kResThreads, 0, s>>>(D, slot, 0);
-    else
-        k_residual<<<res_blocks, T, 0, s>>>(D, slot, 0);
+    launch_residual(slot);
     mark("flux_residual");
     if (D.implicit) {
         for (int c = 0; c < C; ++c) {
@@ -581,6 +590,18 @@ void Solver::Impl::upload_ref4(double4* dst, const double* host)
 {
     h2d(dstage, reinterpret_cast<const double4*>(host), n, s);
     k_to_dev<<<blocks_for(n_pad, 256), 256, 0, s>>>(dst, dstage, D.orig, n_pad);
+}
+
+void Solver::Impl::upload_field(PtRec* dst, int field, const double* host)
+{
+    h2d(dstage, reinterpret_cast<const double4*>(host), n, s);
+    k_ref_to_rec<<<blocks_for(n_pad, 256), 256, 0, s>>>(dst, field, dstage, D.orig, n_pad);
+}
+
+void Solver::Impl::download_field(double* host, const PtRec* src, int field)
+{
+    k_rec_to_ref<<<blocks_for(n_pad, 256), 256, 0, s>>>(dstage, src, field, D.orig, n_pad);
+    d2h(reinterpret_cast<double4*>(host), dstage, n, s);
 }
 
 void Solver::Impl::download_ref4(double* host, const double4* src)
@@ -923,7 +944,7 @@ int Solver::stage_q(const double* U, double* q, std::string& reason, int& point)
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     k_q_from_u<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, 0, 1);
-    I.download_ref4(q, I.D.q);
+    I.download_field(q, I.D.P[0], 0);
     d2h(I.h_status, I.D.status, 1, I.s);
     ck(cudaStreamSynchronize(I.s), "stage_q");
     if (*I.h_status != kNoKey) {
@@ -942,16 +963,17 @@ int Solver::stage_grads(const double* q, double* qx, double* qy)
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    I.upload_ref4(I.D.q, q);
+    I.upload_field(I.D.P[0], 0, q);
+    I.upload_field(I.D.P[1], 0, q);
     I.launch_grad(true, 0, 0);
     int slot = 0;
     for (int pass = 2; pass <= I.cfg.n_inner; ++pass) {
         I.launch_grad(false, slot, slot ^ 1);
         slot ^= 1;
     }
-    I.download_ref4(qx, I.D.qx[slot]);
+    I.download_field(qx, I.D.P[slot], 1);
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.download_ref4(qy, I.D.qy[slot]);
+    I.download_field(qy, I.D.P[slot], 2);
     ck(cudaStreamSynchronize(I.s), "stage_grads");
     return KF_OK;
 }
@@ -965,15 +987,12 @@ int Solver::stage_residual(const double* q, const double* qx, const double* qy, 
     ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    I.upload_ref4(I.D.q, q);
+    I.upload_field(I.D.P[0], 0, q);
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.upload_ref4(I.D.qx[0], qx);
+    I.upload_field(I.D.P[0], 1, qx);
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.upload_ref4(I.D.qy[0], qy);
-    if (I.flux16)
-        k_residual16<2><<<I.res_blocks, kResThreads, 0, I.s>>>(I.D, 0, 0);
-    else
-        k_residual<<<I.res_blocks, kThreads, 0, I.s>>>(I.D, 0, 0);
+    I.upload_field(I.D.P[0], 2, qy);
+    I.launch_residual(0);
     I.download_ref4(R, I.D.R);
     ck(cudaStreamSynchronize(I.s), "sync");
     if (demoted) {
