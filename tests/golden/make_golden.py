@@ -119,7 +119,9 @@ def main():
                         counters=res.counters, diverged=np.array(res.diverged),
                         abort_reason=np.array(res.abort_reason),
                         final_state_sha=np.array(sha(res.final_state)),
-                        final_state_rows=res.final_state[::97].copy())
+                        final_state_rows=res.final_state[::97].copy(),
+                        state400_rows=ref.run(variant="manish_ad", n_iterations=400, mach=0.63,
+                                              aoa_deg=2.0, cfl=0.2).final_state[::97].copy())
     print("config1", len(res.residual), res.abort_reason)
 
     # short histories of every variant on the small cloud (counters included)
