@@ -247,7 +247,7 @@ void kf_config_default(kf_config* cfg)
     cfg->cfl_start = 0.0;
     cfg->divergence_factor = 1e6;
     cfg->device = 0;
-    cfg->ordering = 0;
+    cfg->ordering = 1;
     cfg->use_graph = 1;
 }
 

@@ -222,6 +222,21 @@ void split_weights(Cloud& c, int slot, bool axis_x, int p, bool& flagged)
     const int cls = classify_moments(mo, m);
     c.split_class[slot][p] = cls;
     c.ls_one[slot][p] = 0.0;
+    const int l = 2 + slot;
+    c.coefA[l][p] = 0.0;
+    c.coefB[l][p] = 0.0;
+    c.coefD[l][p] = 1.0;
+    if (cls == kLineX && axis_x) {
+        c.coefA[l][p] = 1.0;
+        c.coefD[l][p] = mo.xx;
+    } else if (cls == kLineY && !axis_x) {
+        c.coefA[l][p] = 1.0;
+        c.coefD[l][p] = mo.yy;
+    } else if (cls == kRegular) {
+        c.coefA[l][p] = axis_x ? mo.yy : mo.xx;
+        c.coefB[l][p] = mo.xy;
+        c.coefD[l][p] = mo.xx * mo.yy - mo.xy * mo.xy;
+    }
     if (cls == kEmpty) return;
     if (cls == kSingular) {
         flagged = true;
@@ -257,6 +272,11 @@ void ls_operators(Cloud& c)
         c.ls_one[s].assign(c.n, 0.0);
         c.split_class[s].assign(c.n, kEmpty);
     }
+    for (int l = 0; l < 6; ++l) {
+        c.coefA[l].assign(c.n, 0.0);
+        c.coefB[l].assign(c.n, 0.0);
+        c.coefD[l].assign(c.n, 1.0);
+    }
     c.flagged.clear();
     for (int p = 0; p < c.n; ++p) {
         bool flagged = false;
@@ -267,6 +287,12 @@ void ls_operators(Cloud& c)
         c.full_class[p] = cls;
         if (cls == kRegular) {
             const double den = mo.xx * mo.yy - mo.xy * mo.xy;
+            c.coefA[0][p] = mo.yy;
+            c.coefB[0][p] = mo.xy;
+            c.coefD[0][p] = den;
+            c.coefA[1][p] = mo.xx;
+            c.coefB[1][p] = mo.xy;
+            c.coefD[1][p] = den;
             for (int k = 0; k < m; ++k) {
                 const double dx = c.x[st[k]] - c.x[p];
                 const double dy = c.y[st[k]] - c.y[p];
@@ -274,8 +300,12 @@ void ls_operators(Cloud& c)
                 c.wy[b + k] = (mo.xx * dy - mo.xy * dx) / den;
             }
         } else if (cls == kLineX) {
+            c.coefA[0][p] = 1.0;
+            c.coefD[0][p] = mo.xx;
             for (int k = 0; k < m; ++k) c.wx[b + k] = (c.x[st[k]] - c.x[p]) / mo.xx;
         } else if (cls == kLineY) {
+            c.coefA[1][p] = 1.0;
+            c.coefD[1][p] = mo.yy;
             for (int k = 0; k < m; ++k) c.wy[b + k] = (c.y[st[k]] - c.y[p]) / mo.yy;
         } else if (cls == kSingular) {
             flagged = true;

@@ -44,6 +44,15 @@ struct Cloud {
     std::vector<double> ls_one[4];     // per point
     std::vector<int> split_class[4];   // per point
     std::vector<int> flagged;          // points owning a Singular stencil
+    // The same weights as per-point linear forms of the entry offset, so the
+    // device can rebuild them from gathered coordinates instead of streaming
+    // them per entry: list l (0 full-x, 1 full-y, 2+slot split) gives
+    //   x-form (l = 0, 2+kXpos, 2+kXneg): w = (A*dx - B*dy) / D
+    //   y-form (l = 1, 2+kYpos, 2+kYneg): w = (A*dy - B*dx) / D
+    // which is the reference's expression term for term (spatial.cpp:64-73,
+    // 102-115), hence bitwise the stored weight; lists with no weights have
+    // A = B = 0, D = 1.
+    std::vector<double> coefA[6], coefB[6], coefD[6];
 
     // StencilReport (pointcloud.hpp:21-26)
     std::vector<int> empty_points, singular_points;

@@ -158,6 +158,7 @@ struct Solver::Impl {
     long long total_counters[5] = {0, 0, 0, 0, 0};
     int forces_err = 0;
     int res_blocks = 0;
+    int n_tile_blocks = 0;
     int flux_variant = 0;  // residual kernel: 0 exact/3 blocks, 1 exact/4, 2 fast/3, 3 fast/4
     int launches = 0;
     int launches_bench = 0;
@@ -172,9 +173,9 @@ struct Solver::Impl {
     void launch_grad(bool first, int src, int dst)
     {
         if (first)
-            k_grad<true><<<blocks_for(n_pad, kThreads), kThreads, 0, s>>>(D, src, dst);
+            k_grad<true><<<n_tile_blocks, kThreads, 0, s>>>(D, src, dst);
         else
-            k_grad<false><<<blocks_for(n_pad, kThreads), kThreads, 0, s>>>(D, src, dst);
+            k_grad<false><<<n_tile_blocks, kThreads, 0, s>>>(D, src, dst);
     }
     void launch_residual(int gslot)
     {
@@ -277,21 +278,40 @@ void Solver::Impl::pack(const Cloud& c)
         slice_off[sl + 1] = slice_off[sl] + 32 * w;
     }
     const size_t n_e = static_cast<size_t>(slice_off[n_slices]);
-    // slots past a point's degree refer to the point itself with zero weights
-    std::vector<int> e_nbr(n_e, 0);
+    if (n_pad > static_cast<int>(kIdMask))
+        throw SolverError(KF_CONFIG, "cloud too large for 28-bit stencil entries");
+    // slots past a point's degree refer to the point itself with an empty mask
+    std::vector<unsigned> e_id(n_e, 0u);
     for (int pn = 0; pn < n_pad; ++pn)
         for (size_t e = slice_off[pn >> 5] + (pn & 31); e < static_cast<size_t>(slice_off[(pn >> 5) + 1]); e += 32)
-            e_nbr[e] = pn;
-    std::vector<double2> e_wxy(n_e, make_double2(0, 0));
-    std::vector<double4> e_w4(n_e, make_double4(0, 0, 0, 0));
+            e_id[e] = static_cast<unsigned>(pn);
+    // LS linear forms in device direction order d = X+ (xneg), X- (xpos),
+    // Y+ (yneg), Y- (ypos); split slot of each direction:
+    const int slot_of[4] = {kXneg, kXpos, kYneg, kYpos};
+    std::vector<double4> lsf(n_pad, make_double4(0, 0, 0, 0)), lsA(n_pad, make_double4(0, 0, 0, 0)),
+        lsB(n_pad, make_double4(0, 0, 0, 0)), lsD(n_pad, make_double4(1, 1, 1, 1));
+    std::vector<double2> lsfd(n_pad, make_double2(1, 1)), xy(n_pad, make_double2(0, 0));
+    auto form = [](double A, double B, double Dn, double u, double v) { return (A * u - B * v) / Dn; };
     nnz_w = 0;
     for (int pn = 0; pn < n_pad; ++pn) {
         const int o = perm[pn];
         if (o < 0) continue;
         kind[pn] = static_cast<signed char>(c.kind[o]);
         nrm[pn] = make_double2(c.nx[o], c.ny[o]);
+        xy[pn] = make_double2(c.x[o], c.y[o]);
         lsone[pn] = make_double4(c.ls_one[kXpos][o], c.ls_one[kXneg][o], c.ls_one[kYpos][o],
                                  c.ls_one[kYneg][o]);
+        lsf[pn] = make_double4(c.coefA[0][o], c.coefB[0][o], c.coefA[1][o], c.coefB[1][o]);
+        lsfd[pn] = make_double2(c.coefD[0][o], c.coefD[1][o]);
+        double cA[4], cB[4], cD[4];
+        for (int d = 0; d < 4; ++d) {
+            cA[d] = c.coefA[2 + slot_of[d]][o];
+            cB[d] = c.coefB[2 + slot_of[d]][o];
+            cD[d] = c.coefD[2 + slot_of[d]][o];
+        }
+        lsA[pn] = make_double4(cA[0], cA[1], cA[2], cA[3]);
+        lsB[pn] = make_double4(cB[0], cB[1], cB[2], cB[3]);
+        lsD[pn] = make_double4(cD[0], cD[1], cD[2], cD[3]);
         unsigned char ne = 0;
         if (c.split[kXneg].degree(o)) ne |= 1;
         if (c.split[kXpos].degree(o)) ne |= 2;
@@ -313,14 +333,14 @@ void Solver::Impl::pack(const Cloud& c)
                 best_d = dist;
                 best = i;
             }
-            const int kk = k - c.nbr.off[o];
-            const size_t e = static_cast<size_t>(slice_off[pn >> 5]) + 32 * kk + (pn & 31);
-            e_nbr[e] = inv[i];
-            e_wxy[e] = make_double2(c.wx[k], c.wy[k]);
+            // the linear forms must reproduce the stored weights bit for bit
+            if (form(c.coefA[0][o], c.coefB[0][o], c.coefD[0][o], dx, dy) != c.wx[k] ||
+                form(c.coefA[1][o], c.coefB[1][o], c.coefD[1][o], dy, dx) != c.wy[k])
+                throw SolverError(KF_RUNTIME, "LS linear form does not reproduce the full-stencil weight");
             // the split-list entries that this full-stencil entry became
             // (pointcloud.cpp:281-289 appends in nbr order)
-            double w[4] = {0, 0, 0, 0};  // xpos, xneg, ypos, yneg
-            const bool in[4] = {dx >= 0.0, dx <= 0.0, dy >= 0.0, dy <= 0.0};
+            const bool in[4] = {dx >= 0.0, dx <= 0.0, dy >= 0.0, dy <= 0.0};  // slot order
+            double w[4] = {0, 0, 0, 0};
             for (int sidx = 0; sidx < 4; ++sidx) {
                 if (!in[sidx]) continue;
                 const int pos = c.split[sidx].off[o] + cnt[sidx]++;
@@ -328,11 +348,47 @@ void Solver::Impl::pack(const Cloud& c)
                     throw SolverError(KF_RUNTIME, "split stencil / neighbour order mismatch");
                 w[sidx] = c.split_w[sidx][pos];
             }
-            e_w4[e] = make_double4(w[kXneg], w[kXpos], w[kYneg], w[kYpos]);
-            nnz_w += (w[0] != 0.0) + (w[1] != 0.0) + (w[2] != 0.0) + (w[3] != 0.0);
+            unsigned mask = 0;
+            for (int d = 0; d < 4; ++d) {
+                const double wd = w[slot_of[d]];
+                if (wd == 0.0) continue;
+                mask |= 1u << d;
+                const double f = d < 2 ? form(cA[d], cB[d], cD[d], dx, dy) : form(cA[d], cB[d], cD[d], dy, dx);
+                if (f != wd)
+                    throw SolverError(KF_RUNTIME, "LS linear form does not reproduce a split weight");
+            }
+            const int kk = k - c.nbr.off[o];
+            const size_t e = static_cast<size_t>(slice_off[pn >> 5]) + 32 * kk + (pn & 31);
+            e_id[e] = static_cast<unsigned>(inv[i]) | (mask << 28);
+            nnz_w += __builtin_popcount(mask);
         }
         hmin[pn] = h;
         if (c.kind[o] == kOuter) near_int[pn] = best >= 0 ? inv[best] : -1;
+    }
+    // processing order of the point-parallel kernels: slices sorted by the
+    // Morton code of their first point, so the resident front of a launch is
+    // spatially compact across all colours (L2 reuse of the gathers)
+    std::vector<int> tiles;
+    {
+        const double x0 = *std::min_element(c.x.begin(), c.x.end());
+        const double x1 = *std::max_element(c.x.begin(), c.x.end());
+        const double y0 = *std::min_element(c.y.begin(), c.y.end());
+        const double y1 = *std::max_element(c.y.begin(), c.y.end());
+        const double sx = x1 > x0 ? 4294967295.0 / (x1 - x0) : 0.0;
+        const double sy = y1 > y0 ? 4294967295.0 / (y1 - y0) : 0.0;
+        std::vector<std::pair<uint64_t, int>> key;
+        for (int sl = 0; sl < n_slices; ++sl) {
+            const int o = perm[sl * 32];
+            if (o < 0) continue;
+            key.emplace_back(morton2(static_cast<uint32_t>((c.x[o] - x0) * sx),
+                                     static_cast<uint32_t>((c.y[o] - y0) * sy)),
+                             sl);
+        }
+        std::stable_sort(key.begin(), key.end());
+        for (auto& kv : key) tiles.push_back(kv.second);
+        while (tiles.size() % (kThreads / 32)) tiles.push_back(-1);
+        if (tiles.empty())
+            for (int k = 0; k < kThreads / 32; ++k) tiles.push_back(-1);
     }
     // ---- wall loop geometry for compute_forces (driver.cpp:127-167)
     const int W = static_cast<int>(c.wall_ids.size());
@@ -428,15 +484,29 @@ void Solver::Impl::pack(const Cloud& c)
     int* d_soff = dalloc<int>(slice_off.size(), owned);
     up(d_soff, slice_off);
     D.slice_off = d_soff;
-    int* d_enbr = dalloc<int>(n_e, owned);
-    up(d_enbr, e_nbr);
-    D.e_nbr = d_enbr;
-    double2* d_ewxy = dalloc<double2>(n_e, owned);
-    up(d_ewxy, e_wxy);
-    D.e_wxy = d_ewxy;
-    double4* d_ew4 = dalloc<double4>(n_e, owned);
-    up(d_ew4, e_w4);
-    D.e_w4 = d_ew4;
+    unsigned* d_eid = dalloc<unsigned>(n_e, owned);
+    up(d_eid, e_id);
+    D.e_id = d_eid;
+    auto up4 = [&](const std::vector<double4>& h) {
+        double4* d = dalloc<double4>(h.size(), owned);
+        up(d, h);
+        return static_cast<const double4*>(d);
+    };
+    auto up2 = [&](const std::vector<double2>& h) {
+        double2* d = dalloc<double2>(h.size(), owned);
+        up(d, h);
+        return static_cast<const double2*>(d);
+    };
+    D.lsf = up4(lsf);
+    D.lsfd = up2(lsfd);
+    D.lsA = up4(lsA);
+    D.lsB = up4(lsB);
+    D.lsD = up4(lsD);
+    D.xy = up2(xy);
+    int* d_tiles = dalloc<int>(tiles.size(), owned);
+    up(d_tiles, tiles);
+    D.tiles = d_tiles;
+    n_tile_blocks = static_cast<int>(tiles.size()) / (kThreads / 32);
 
     for (int b = 0; b < 2; ++b) {
         D.U[b] = dalloc<double4>(n_pad, owned);
@@ -470,7 +540,7 @@ void Solver::Impl::pack(const Cloud& c)
         const std::string v = env ? env : "m3";
         flux_variant = v == "m4" ? 1 : v == "m3fast" ? 2 : v == "m4fast" ? 3 : 0;
     }
-    res_blocks = blocks_for(n_pad, kThreads);
+    res_blocks = n_tile_blocks;
     D.res_part = dalloc<double>(res_blocks, owned);
     D.cnt_part = dalloc<long long>(res_blocks, owned);
     D.fo_part = dalloc<int>(res_blocks, owned);
