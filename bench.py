@@ -19,9 +19,16 @@ and dU_prev is inside the timed step).
           kf_step_host with pinned HOST buffers: H2D(U, dU_prev) + iteration +
           D2H(U', dU, record) every step.
 
-Multi-GPU (--gpus N under torchrun): "replicas only" for now — each rank
-solves its own copy of the cloud (weak scaling, no data-path collective);
-the partitioned solver with halo exchange is future work.
+Multi-GPU (--gpus N under torchrun, one process per GPU): the domain-
+decomposed solver. The cloud grows with N (n_wall = 1280 N,
+so every GPU owns ~640,000 points: weak scaling), is cut into N angular
+wedges, and every rank solves its wedge with ghost points refreshed by grouped
+ncclSend/ncclRecv between dependent stages plus one ncclAllReduce of the
+residual/forces/abort partials per iteration. `value` is all ranks' points
+times steps over the max-over-ranks device time.
+
+--parts P (single process) runs the same decomposition in-process on one GPU
+(ghosts refreshed by device copies): the partitioning overhead on one B200.
 
 --impl reference times the reference's own CPU solver (oracle/_ref, all host
 threads) on the same case.
@@ -149,12 +156,24 @@ def reference_cpu(n_iters_total, threads, spec=CASE):
     return secs[:n_iters_total], ctx.n, kind
 
 
+def case_for(world, points=None):
+    """The bench workload at `world` GPUs: config 2 at N=1; the cloud grows
+    with N in the wall direction (weak scaling, ~640,000 points per GPU)."""
+    spec = dict(CASE)
+    spec["n_wall"] = CASE["n_wall"] * max(world, 1)
+    if points:
+        nw, nr = points.split(":")
+        spec["n_wall"], spec["n_radial"] = int(nw), int(nr)
+    return spec
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     threads = cpu_cores()
-    secs, n, kind = reference_cpu(args.warmup + args.steps, threads)
+    spec = case_for(world, args.points)
+    secs, n, kind = reference_cpu(args.warmup + args.steps, threads, spec)
     timed = secs[args.warmup:args.warmup + args.steps] or secs
     total = float(np.sum(timed))
     value = n * len(timed) / total / 1e6
@@ -163,7 +182,8 @@ def run_reference_arm(args):
         "steps": len(timed), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(timed),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated NACA 0012 O-grid, deterministic)",
-        "config": {"workload": "naca0012:1280:500:20 M0.85 AoA1 manish_ad CFL0.2, one fixed-point iteration",
+        "config": {"workload": f"naca0012:{spec['n_wall']}:{spec['n_radial']}:20 M0.85 AoA1 manish_ad CFL0.2, "
+                               "one fixed-point iteration",
                    "points": n, "parallelism": "cpu-openmp"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{len(timed)} reference iterations of the same case (runs restarted "
@@ -184,6 +204,7 @@ def main():
     ap.add_argument("--profile-only", action="store_true",
                     help="run a few steps for ncu (no JSON line)")
     ap.add_argument("--points", default=None, help="override cloud n_wall:n_radial")
+    ap.add_argument("--parts", type=int, default=1, help="in-process partitions on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -198,16 +219,18 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    spec = dict(CASE)
-    if args.points:
-        nw, nr = args.points.split(":")
-        spec["n_wall"], spec["n_radial"] = int(nw), int(nr)
+    spec = case_for(world, args.points)
 
     cloud = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
     N = cloud.n()
     cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(spec["variant"]), mach_inf=spec["mach"],
                           aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=64, device=local)
-    solver = kf.Solver(cloud, cfg)
+    if world > 1:
+        ids = [kf.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(ids, src=0)
+        solver = kf.Solver.for_rank(cloud, cfg, world, rank, ids[0])
+    else:
+        solver = kf.Solver(cloud, cfg, n_parts=args.parts)
     solver.reset()
     solver.iterate_async(WARM_ITERS)
     recs, st = solver.sync_records()
@@ -244,7 +267,7 @@ def main():
     if world > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    value = N * args.steps * world / (ms_max * 1e-3) / 1e6
+    value = N * args.steps / (ms_max * 1e-3) / 1e6  # N: points of the whole (all-rank) cloud
     launches = solver.launches_per_iteration * args.steps
 
     # ---- end to end through the C ABI with pinned host buffers
@@ -281,7 +304,17 @@ def main():
     et = torch.tensor([e2e_ms], device="cuda")
     if world > 1:
         torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = N * args.steps * world / (float(et.item()) * 1e-3) / 1e6
+    e2e_value = N * args.steps / (float(et.item()) * 1e-3) / 1e6
+
+    if world > 1:
+        # each rank moves only its own (+ghost) points across PCIe
+        n_loc = solver.owned_points
+        bt = torch.tensor([n_loc * 64, n_loc * 64 + C.sizeof(rec)], device="cuda", dtype=torch.int64)
+        torch.distributed.all_reduce(bt)
+        h2d_b, d2h_b = int(bt[0].item()), int(bt[1].item())
+    else:
+        h2d_b = int(Uh.numel() * 8 + dUh.numel() * 8)
+        d2h_b = int(Uo.numel() * 8 + dUo.numel() * 8 + C.sizeof(rec))
 
     # ---- per-kernel profile (CUDA events between launches) for the roofline
     prof = solver.profile_kernels(reps=5)
@@ -294,7 +327,8 @@ def main():
     flux_ms = agg["flux_residual"][1]
     ls = kf.build_ls_coefficients(cloud)
     n_s = float(sum(np.count_nonzero(ls.split_w[k]) for k in ls.split_w)) / N
-    flux_bytes = N * (FLUX_BYTES_FIXED + 4.0 * n_s)
+    n_own = solver.owned_points  # the flux kernels of this rank's partition(s)
+    flux_bytes = n_own * (FLUX_BYTES_FIXED + 4.0 * n_s)
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
@@ -307,7 +341,7 @@ def main():
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            if tj.get("points") == N:
+            if tj.get("points") == N and world == 1 and args.parts == 1:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -319,14 +353,14 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
         "config": {
-            "workload": "naca0012:1280:500:20 M0.85 AoA1 manish_ad CFL0.2 n_inner3, one fixed-point "
-                        "iteration (re-run of iteration 6 from the resident iteration-5 state)",
+            "workload": f"naca0012:{spec['n_wall']}:{spec['n_radial']}:20 M0.85 AoA1 manish_ad CFL0.2 n_inner3, "
+                        "one fixed-point iteration (re-run of iteration 6 from the resident iteration-5 state)",
             "points": N, "colours": int(kf.color_points(cloud).n_colors),
-            "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+            "parallelism": (f"domain-decomposition x{world} (angular wedges, NCCL halos)" if world > 1 else
+                            f"single-gpu, {args.parts} in-process partitions" if args.parts > 1 else "single-gpu"),
             "l2": "inputs larger than L2 (per-iteration working set > 400 MB vs 126 MB L2)",
         },
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(Uh.numel() * 8 + dUh.numel() * 8),
-                "d2h_bytes_per_step": int(Uo.numel() * 8 + dUo.numel() * 8 + C.sizeof(rec)),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                 "call": "kf_step_host (C ABI, pinned host buffers)"},
         "gpu_launches": launches,
         "clocks": clocks,
@@ -344,7 +378,7 @@ def main():
                   "cl": recs[WARM_ITERS].cl if len(recs) > WARM_ITERS else None},
     }
     if rank == 0 and not args.no_cpu_baseline:
-        secs, n_ref, kind = reference_cpu(8, cpu_cores())
+        secs, n_ref, kind = reference_cpu(8, cpu_cores(), spec)
         secs = secs[1:] or secs
         line["cpu_baseline"] = {
             "value": n_ref / float(np.median(secs)) / 1e6, "unit": UNIT, "cores": cpu_cores(),

@@ -14,6 +14,7 @@ from .api import (  # noqa: F401
     InvalidStateError,
     IterationRecord,
     KinfreeError,
+    LocalLayout,
     LsCoefficients,
     PointCloud,
     PointKind,
@@ -31,6 +32,8 @@ from .api import (  # noqa: F401
     jvp_split,
     load_cloud,
     measure_fp64_peak,
+    nccl_unique_id,
+    partition_plan,
     run_fixed_point,
     save_cloud,
     set_colors,

@@ -28,7 +28,13 @@ EXPORTED = [
     "kf_stage_residual", "kf_stage_lusgs", "kf_stage_update", "kf_stage_forces",
     "kf_probe_split_flux", "kf_probe_jvp_split", "kf_probe_jvp_full", "kf_version",
     "kf_device_count", "kf_profile_kernels", "kf_measure_fp64_peak",
+    "kf_partition_plan", "kf_layout_build", "kf_layout_free", "kf_layout_sizes",
+    "kf_layout_arrays", "kf_layout_send", "kf_layout_recv", "kf_create_partitioned",
+    "kf_nccl_unique_id", "kf_create_rank", "kf_n_parts", "kf_owned_points",
 ]
+
+KF_NCCL_ID_BYTES = 128
+KF_PART_ANGULAR, KF_PART_MORTON = 0, 1
 
 
 class Status(C.Structure):
@@ -109,6 +115,19 @@ def _load():
         "kf_probe_jvp_full": (_S, [C.c_int, _dp, _dp, C.c_int, C.c_int, _dp]),
         "kf_profile_kernels": (_S, [_vp, C.c_int, C.c_char_p, _vp, C.c_int, C.POINTER(C.c_int)]),
         "kf_measure_fp64_peak": (_S, [C.c_int, C.POINTER(C.c_double)]),
+        "kf_partition_plan": (_S, [_vp, C.c_int, C.c_int, _ip]),
+        "kf_layout_build": (_S, [_vp, _ip, C.c_int, C.c_int, C.c_int, _pp]),
+        "kf_layout_free": (None, [_vp]),
+        "kf_layout_sizes": (None, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_int)]),
+        "kf_layout_arrays": (None, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+        "kf_layout_send": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),
+        "kf_layout_recv": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+        "kf_create_partitioned": (_S, [_vp, C.POINTER(Config), C.c_int, C.c_int, _pp]),
+        "kf_nccl_unique_id": (_S, [C.c_char_p]),
+        "kf_create_rank": (_S, [_vp, C.POINTER(Config), C.c_int, C.c_int, C.c_int, C.c_char_p, _pp]),
+        "kf_n_parts": (C.c_int, [_vp]),
+        "kf_owned_points": (C.c_int, [_vp]),
         "kf_version": (C.c_char_p, []),
         "kf_device_count": (C.c_int, []),
     }

@@ -395,17 +395,61 @@ def _records(buf, n):
 
 
 # ------------------------------------------------------------------ solver
-class Solver:
-    """A device context (kf_ctx): one uploaded cloud + configuration."""
+_PART_MODES = {"angular": L.KF_PART_ANGULAR, "morton": L.KF_PART_MORTON}
 
-    def __init__(self, cloud: PointCloud, config: SolverConfig):
+
+def _part_mode(mode) -> int:
+    if isinstance(mode, str):
+        if mode not in _PART_MODES:
+            raise ValueError(f"unknown partition mode '{mode}'")
+        return _PART_MODES[mode]
+    return int(mode)
+
+
+class Solver:
+    """A device context (kf_ctx): one uploaded cloud + configuration.
+
+    ``n_parts > 1`` splits the cloud into that many partitions held by this
+    process on ``config.device`` (the domain-decomposed solver, halos
+    refreshed by device copies); ``Solver.for_rank`` is the one-process-per-GPU
+    form over NCCL.
+    """
+
+    def __init__(self, cloud: PointCloud, config: SolverConfig, n_parts: int = 1,
+                 partition="angular", _rank=None):
         self.cloud = cloud
         self.config = config
         self.n = cloud.n()
         self._cfg = config.to_c()
         h = C.c_void_p()
-        _check(lib.kf_create(cloud.handle, C.byref(self._cfg), C.byref(h)))
+        if _rank is not None:
+            n_ranks, rank, nccl_id = _rank
+            _check(lib.kf_create_rank(cloud.handle, C.byref(self._cfg), n_ranks, rank, _part_mode(partition),
+                                      nccl_id, C.byref(h)))
+        elif n_parts == 1:
+            _check(lib.kf_create(cloud.handle, C.byref(self._cfg), C.byref(h)))
+        else:
+            _check(lib.kf_create_partitioned(cloud.handle, C.byref(self._cfg), n_parts,
+                                             _part_mode(partition), C.byref(h)))
         self._h = h
+
+    @classmethod
+    def for_rank(cls, cloud: PointCloud, config: SolverConfig, n_ranks: int, rank: int,
+                 nccl_id: bytes, partition="angular") -> "Solver":
+        """Partition `rank` of an `n_ranks`-way decomposition, one process per
+        GPU; every rank passes the same cloud, config and NCCL id
+        (``nccl_unique_id()`` on rank 0, broadcast by the caller). Host state
+        arrays keep the whole-cloud shape; only this rank's owned entries are
+        written."""
+        return cls(cloud, config, partition=partition, _rank=(n_ranks, rank, nccl_id))
+
+    @property
+    def n_parts(self) -> int:
+        return lib.kf_n_parts(self._h)
+
+    @property
+    def owned_points(self) -> int:
+        return lib.kf_owned_points(self._h)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -523,6 +567,59 @@ class Solver:
         cl, cd = C.c_double(), C.c_double()
         _check(lib.kf_stage_forces(self._h, _f64(U, (self.n, 4)), C.byref(cl), C.byref(cd)))
         return cl.value, cd.value
+
+
+# ------------------------------------------------------ domain decomposition
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 of a multi-process run)."""
+    buf = C.create_string_buffer(L.KF_NCCL_ID_BYTES)
+    _check(lib.kf_nccl_unique_id(buf))
+    return buf.raw
+
+
+def partition_plan(cloud: PointCloud, n_parts: int, mode="angular") -> np.ndarray:
+    """Owner partition of every point (kf_partition_plan)."""
+    owner = np.zeros(cloud.n(), np.int32)
+    _check(lib.kf_partition_plan(cloud.handle, n_parts, _part_mode(mode), owner))
+    return owner
+
+
+class LocalLayout:
+    """Host-side local numbering and halo plan of one partition (kf_layout)."""
+
+    def __init__(self, cloud: PointCloud, owner, n_parts: int, rank: int, ordering: int = 1):
+        h = C.c_void_p()
+        _check(lib.kf_layout_build(cloud.handle, np.ascontiguousarray(owner, np.int32), n_parts, rank,
+                                   ordering, C.byref(h)))
+        self._h = h
+        a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        lib.kf_layout_sizes(h, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
+        self.n_local, self.n_owned, self.n_colors, self.n_peers = a.value, b.value, c.value, d.value
+        self.perm = np.zeros(self.n_local, np.int32)
+        self.ghost = np.zeros(self.n_local, np.uint8)
+        self.gs, self.oe, self.ge = (np.zeros(self.n_colors, np.int32) for _ in range(3))
+        self.peers = np.zeros(max(self.n_peers, 1), np.int32)
+        lib.kf_layout_arrays(h, _ptr(self.perm), _ptr(self.ghost), _ptr(self.gs), _ptr(self.oe),
+                             _ptr(self.ge), _ptr(self.peers))
+        self.peers = self.peers[:self.n_peers]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            lib.kf_layout_free(h)
+            self._h = None
+
+    def send(self, peer_slot: int, color: int) -> np.ndarray:
+        m = lib.kf_layout_send(self._h, peer_slot, color, None)
+        out = np.zeros(max(m, 0), np.int32)
+        if m > 0:
+            lib.kf_layout_send(self._h, peer_slot, color, _ptr(out))
+        return out
+
+    def recv(self, peer_slot: int, color: int):
+        off = C.c_int()
+        m = lib.kf_layout_recv(self._h, peer_slot, color, C.byref(off))
+        return off.value, m
 
 
 def run_fixed_point(cloud: PointCloud, config: SolverConfig, colors=None) -> RunHistory:

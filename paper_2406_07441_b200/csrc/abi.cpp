@@ -10,10 +10,15 @@
 
 #include "../../include/kf.h"
 #include "cloud.hpp"
+#include "partition.hpp"
 #include "solver.hpp"
 
 struct kf_cloud {
     kfb::Cloud c;
+};
+
+struct kf_layout {
+    kfb::LocalLayout L;
 };
 
 struct kf_ctx {
@@ -251,7 +256,12 @@ void kf_config_default(kf_config* cfg)
     cfg->use_graph = 1;
 }
 
-kf_status kf_create(const kf_cloud* cloud, const kf_config* cfg, kf_ctx** out)
+}  // extern "C"
+
+namespace {
+
+kf_status create_ctx(const kf_cloud* cloud, const kf_config* cfg, const kfb::PartitionSpec& spec,
+                     kf_ctx** out)
 {
     return guarded([&] {
         *out = nullptr;
@@ -260,6 +270,9 @@ kf_status kf_create(const kf_cloud* cloud, const kf_config* cfg, kf_ctx** out)
         if (cfg->n_iterations < 1) return err(KF_CONFIG, "n_iterations must be >= 1");
         if (cfg->n_inner < 1) return err(KF_CONFIG, "q_derivatives: n_inner must be >= 1");
         if (cfg->variant < 0 || cfg->variant > 4) return err(KF_CONFIG, "unknown variant");
+        if (spec.n_parts < 1) return err(KF_CONFIG, "n_parts must be >= 1");
+        if (spec.mode != kfb::kPartAngular && spec.mode != kfb::kPartMorton)
+            return err(KF_CONFIG, "unknown partition mode");
         const kfb::Cloud& c = cloud->c;
         for (int p : c.flagged)
             if (c.kind[p] == kfb::kInterior)
@@ -270,7 +283,7 @@ kf_status kf_create(const kf_cloud* cloud, const kf_config* cfg, kf_ctx** out)
         try {
             ctx->cfg = *cfg;
             ctx->n = c.n;
-            ctx->solver.reset(new kfb::Solver(c, *cfg));
+            ctx->solver.reset(new kfb::Solver(c, *cfg, spec));
         } catch (...) {
             delete ctx;
             throw;
@@ -278,6 +291,126 @@ kf_status kf_create(const kf_cloud* cloud, const kf_config* cfg, kf_ctx** out)
         *out = ctx;
         return ok();
     });
+}
+
+}  // namespace
+
+extern "C" {
+
+kf_status kf_create(const kf_cloud* cloud, const kf_config* cfg, kf_ctx** out)
+{
+    return create_ctx(cloud, cfg, kfb::PartitionSpec(), out);
+}
+
+kf_status kf_create_partitioned(const kf_cloud* cloud, const kf_config* cfg, int n_parts, int mode,
+                                kf_ctx** out)
+{
+    kfb::PartitionSpec spec;
+    spec.n_parts = n_parts;
+    spec.mode = mode;
+    return create_ctx(cloud, cfg, spec, out);
+}
+
+kf_status kf_nccl_unique_id(unsigned char* id)
+{
+    return guarded([&] {
+        kfb::nccl_unique_id(id);
+        return ok();
+    });
+}
+
+kf_status kf_create_rank(const kf_cloud* cloud, const kf_config* cfg, int n_ranks, int rank, int mode,
+                         const unsigned char* nccl_id, kf_ctx** out)
+{
+    kfb::PartitionSpec spec;
+    spec.n_parts = n_ranks;
+    spec.mode = mode;
+    spec.nccl = n_ranks > 1;
+    spec.rank = rank;
+    spec.nccl_id = nccl_id;
+    if (n_ranks > 1 && !nccl_id) {
+        *out = nullptr;
+        return err(KF_CONFIG, "kf_create_rank: missing NCCL unique id");
+    }
+    if (n_ranks == 1 && rank != 0) {
+        *out = nullptr;
+        return err(KF_CONFIG, "rank out of range");
+    }
+    return create_ctx(cloud, cfg, spec, out);
+}
+
+int kf_n_parts(const kf_ctx* ctx) { return ctx->solver->n_parts(); }
+int kf_owned_points(const kf_ctx* ctx) { return ctx->solver->owned_points(); }
+
+kf_status kf_partition_plan(const kf_cloud* c, int n_parts, int mode, int* owner)
+{
+    return guarded([&] {
+        const std::vector<int> o = kfb::plan_partition(c->c, n_parts, mode);
+        std::memcpy(owner, o.data(), o.size() * sizeof(int));
+        return ok();
+    });
+}
+
+kf_status kf_layout_build(const kf_cloud* c, const int* owner, int n_parts, int rank, int ordering,
+                          kf_layout** out)
+{
+    return guarded([&] {
+        *out = nullptr;
+        std::vector<int> o(owner, owner + c->c.n);
+        for (int v : o)
+            if (v < 0 || v >= n_parts) return err(KF_CONFIG, "owner out of range");
+        auto* L = new kf_layout;
+        try {
+            L->L = kfb::build_local_layout(c->c, o, n_parts, rank, ordering);
+        } catch (...) {
+            delete L;
+            throw;
+        }
+        *out = L;
+        return ok();
+    });
+}
+
+void kf_layout_free(kf_layout* L) { delete L; }
+
+void kf_layout_sizes(const kf_layout* L, int* n_local, int* n_owned, int* n_colors, int* n_peers)
+{
+    if (n_local) *n_local = static_cast<int>(L->L.perm.size());
+    if (n_owned) *n_owned = L->L.n_owned;
+    if (n_colors) *n_colors = L->L.n_colors;
+    if (n_peers) *n_peers = static_cast<int>(L->L.peers.size());
+}
+
+void kf_layout_arrays(const kf_layout* L, int* perm, unsigned char* ghost, int* gs, int* oe, int* ge,
+                      int* peers)
+{
+    const kfb::LocalLayout& l = L->L;
+    if (perm) std::memcpy(perm, l.perm.data(), l.perm.size() * sizeof(int));
+    if (ghost) std::memcpy(ghost, l.ghost.data(), l.ghost.size());
+    if (gs) std::memcpy(gs, l.gs.data(), l.gs.size() * sizeof(int));
+    if (oe) std::memcpy(oe, l.oe.data(), l.oe.size() * sizeof(int));
+    if (ge) std::memcpy(ge, l.ge.data(), l.ge.size() * sizeof(int));
+    if (peers && !l.peers.empty()) std::memcpy(peers, l.peers.data(), l.peers.size() * sizeof(int));
+}
+
+int kf_layout_send(const kf_layout* L, int peer_slot, int color, int* gids)
+{
+    const kfb::LocalLayout& l = L->L;
+    if (peer_slot < 0 || peer_slot >= static_cast<int>(l.peers.size()) || color < 0 || color >= l.n_colors)
+        return -1;
+    const std::vector<int>& v = l.send_idx[peer_slot][color];
+    if (gids)
+        for (size_t k = 0; k < v.size(); ++k) gids[k] = l.perm[v[k]];
+    return static_cast<int>(v.size());
+}
+
+int kf_layout_recv(const kf_layout* L, int peer_slot, int color, int* local_off)
+{
+    const kfb::LocalLayout& l = L->L;
+    if (peer_slot < 0 || peer_slot >= static_cast<int>(l.peers.size()) || color < 0 || color >= l.n_colors)
+        return -1;
+    if (local_off) *local_off = l.recv_off[peer_slot][color];
+    return l.recv_cnt[peer_slot][color];
 }
 
 void kf_destroy(kf_ctx* ctx) { delete ctx; }

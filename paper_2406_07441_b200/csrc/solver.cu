@@ -1,6 +1,22 @@
 // Device solver context: packing of the ingested cloud into the B200 layout,
 // the per-iteration launch sequence (captured as CUDA graphs), the
-// run_fixed_point loop, and the per-stage parity hooks.
+// run_fixed_point loop, the per-stage parity hooks, and the domain-decomposed
+// (partitioned) run of SURVEY.md §8(e).
+//
+// A context holds one or more PARTITIONS of the cloud (partition.hpp). Each
+// partition is a self-contained device layout: its owned points plus ghost
+// copies of their non-owned neighbours, colour-major, so every kernel is the
+// single-GPU kernel. Between dependent stages the ghosts are refreshed by a
+// halo exchange, and the per-iteration reductions (residual norm, tallies,
+// wall Cp, abort keys) are combined across partitions before k_finalize:
+//   * transport "single":   one partition, no exchange (the default path);
+//   * transport "inproc":   P partitions on one device and one stream, ghosts
+//                           filled by device-to-device copies, one shared
+//                           reduction buffer (the parity vehicle on one GPU);
+//   * transport "nccl":     one partition per process / GPU, ghosts filled by
+//                           grouped ncclSend/ncclRecv over NVLink, reductions
+//                           by one ncclAllReduce per iteration.
+// All three run the same kernels and the same exchange schedule.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -9,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <numeric>
 #include <string>
@@ -16,6 +33,8 @@
 
 #include "../../include/kf.h"
 #include "kernels.cuh"
+#include "nccl_dyn.hpp"
+#include "partition.hpp"
 #include "solver.hpp"
 
 namespace kfb {
@@ -53,21 +72,8 @@ int key_stage(unsigned long long k) { return static_cast<int>((k >> 36) & 0xff);
 int key_reason(unsigned long long k) { return static_cast<int>((k >> 32) & 0xf); }
 int key_point(unsigned long long k) { return static_cast<int>(k & 0xffffffffu); }
 
-uint64_t morton2(uint32_t x, uint32_t y)
-{
-    auto spread = [](uint64_t v) {
-        v &= 0xffffffffull;
-        v = (v | (v << 16)) & 0x0000ffff0000ffffull;
-        v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
-        v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
-        v = (v | (v << 2)) & 0x3333333333333333ull;
-        v = (v | (v << 1)) & 0x5555555555555555ull;
-        return v;
-    };
-    return spread(x) | (spread(y) << 1);
-}
-
-// scatter/gather between reference numbering (AoS n x 4) and device order
+// scatter/gather between reference numbering (AoS n x 4) and device order;
+// downloads skip ghosts (kind < 0), uploads fill them too
 __global__ void k_to_dev(double4* dst, const double4* src, const int* orig, int n_pad)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -75,12 +81,13 @@ __global__ void k_to_dev(double4* dst, const double4* src, const int* orig, int 
     const int o = orig[p];
     dst[p] = o >= 0 ? src[o] : make_double4(0, 0, 0, 0);
 }
-__global__ void k_to_ref(double4* dst, const double4* src, const int* orig, int n_pad)
+__global__ void k_to_ref(double4* dst, const double4* src, const int* orig, const signed char* kind,
+                         int n_pad)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n_pad) return;
     const int o = orig[p];
-    if (o >= 0) dst[o] = src[p];
+    if (o >= 0 && kind[p] >= 0) dst[o] = src[p];
 }
 __global__ void k_to_ref1(double* dst, const double* src, const int* orig, int n_pad)
 {
@@ -95,6 +102,17 @@ __global__ void k_to_ref_u8(int* dst, const unsigned char* src, const int* orig,
     if (p >= n_pad) return;
     const int o = orig[p];
     if (o >= 0) dst[o] = src[p];
+}
+// compact <-> local (multi-process transport: only this rank's points cross PCIe)
+__global__ void k_gather_local(double4* dst, const double4* src, const int* idx, int n)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) dst[j] = src[idx[j]];
+}
+__global__ void k_scatter_local(double4* dst, const double4* src, const int* idx, int n)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) dst[idx[j]] = src[j];
 }
 __device__ __forceinline__ double4& rec_field(PtRec& r, int f) { return f == 0 ? r.q : f == 1 ? r.qx : r.qy; }
 __global__ void k_ref_to_rec(PtRec* dst, int field, const double4* src, const int* orig, int n_pad)
@@ -115,7 +133,7 @@ __global__ void k_rec_to_ref(double4* dst, const PtRec* src, int field, const in
 __global__ void k_cp(Dev D, int buf)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= D.n_pad || D.orig[p] < 0 || D.kind[p] != 0 || D.wslot[p] < 0) return;
+    if (p >= D.n_pad || D.kind[p] != 0 || D.wslot[p] < 0) return;
     Prim<double> w;
     if (prim_from_cons(D.U[buf][p], w)) {
         D.cp[D.wslot[p]] = NAN;
@@ -126,25 +144,60 @@ __global__ void k_cp(Dev D, int buf)
 
 int blocks_for(long n, int t) { return static_cast<int>((n + t - 1) / t); }
 
+enum Transport : int { kSingle = 0, kInProc = 1, kNccl = 2 };
+
 }  // namespace
+
+// One partition's device layout and buffers.
+struct Part {
+    int rank = 0;  // partition index (= row of the reduction buffer)
+    int n_pad = 0, n_owned = 0;
+    std::vector<int> gs, oe, ge;
+    std::vector<int> perm;               // local -> global (-1 padding)
+    std::vector<unsigned char> ghost;
+    std::vector<int> own_gid, loc_gid;   // owned / owned+ghost global ids (compact transfers)
+    Dev D{};
+    int n_tile_blocks = 0, res_blocks = 0;
+    long long nnz_w = 0;
+    // halo plan: peers (ascending rank); recv ranges [peer][colour] in local
+    // numbering; send list colour-major, peer-minor: entries of (c, k) at
+    // send_off[c][k] .. + send_cnt[c][k]; colour c spans cstart[c]..cstart[c+1]
+    std::vector<int> peers;
+    std::vector<std::vector<int>> recv_off, recv_cnt;
+    std::vector<std::vector<int>> send_off, send_cnt;
+    std::vector<int> cstart;
+    int n_send = 0;
+    int* d_send = nullptr;
+    PtRec* sendP = nullptr;
+    JRec* sendJ = nullptr;
+    unsigned char* sendB = nullptr;
+    // compact transfers (nccl transport)
+    int* d_own = nullptr;
+    int* d_loc = nullptr;
+    double4* dcomp = nullptr;
+    double4* hcomp = nullptr;  // pinned
+    // bench snapshot
+    double4* Usnap = nullptr;
+    double4* dUsnap = nullptr;
+    // reduction rows + cp (partitioned runs)
+    double* red_local = nullptr;
+    double* red = nullptr;
+};
 
 struct Solver::Impl {
     kf_config cfg{};
-    int n = 0;
-    int n_pad = 0;
+    int n = 0;        // points of the whole cloud
     int C = 0;
-    std::vector<int> gs, ge;
-    std::vector<int> perm;  // new -> orig (-1 padding)
-    Dev D{};
+    int transport = kSingle;
+    int n_rows = 1;   // partitions of the whole run
+    std::vector<Part> parts;
     std::vector<void*> owned;
     cudaStream_t s = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     cudaGraphExec_t bench_graph = nullptr;
     int bench = 0;
     int cur = 0;  // buffer holding the current state
-    double4* dstage = nullptr;   // n x 4 staging (reference order)
-    double4* Usnap = nullptr;
-    double4* dUsnap = nullptr;
+    double4* dstage = nullptr;  // n x 4 staging (reference order)
     int snap_iter = 0;
     double* dstage1 = nullptr;
     int* dstage_i = nullptr;
@@ -153,49 +206,66 @@ struct Solver::Impl {
     std::vector<double> h_init;              // initial state (reference order)
     double4 fsU{};
     std::vector<double> cfl_h;
-    // closed-form counter terms
+    // closed-form counter terms (whole cloud)
     long long nnz_w = 0;
     long long total_counters[5] = {0, 0, 0, 0, 0};
     int forces_err = 0;
-    int res_blocks = 0;
-    int n_tile_blocks = 0;
+    int W = 0;
     int flux_variant = 0;  // residual kernel: 0 exact/3 blocks, 1 exact/4, 2 fast/3, 3 fast/4
     int launches = 0;
     int launches_bench = 0;
     std::vector<DevRecord> rec_h;
     std::vector<cudaEvent_t>* prof_ev = nullptr;
     std::vector<std::string>* prof_names = nullptr;
+    ncclComm_t comm = nullptr;
 
-    Impl(const Cloud& c, const kf_config& cf);
+    Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spec);
     ~Impl();
-    void pack(const Cloud& c);
+    bool multi() const { return n_rows > 1; }
+    Part& p0() { return parts[0]; }
+    void pack(const Cloud& c, const LocalLayout& L, const std::vector<uint64_t>& code,
+              const std::vector<double>& oty, const std::vector<double>& otx, double* red_shared,
+              Part& P);
+    void setup_globals(const Cloud& c, std::vector<double>& oty, std::vector<double>& otx);
     void enqueue_iteration(int cur_buf, double cfl_override, bool with_q);
-    void launch_grad(bool first, int src, int dst)
+    void mark(const char* name);
+    void launch_grad(Part& P, bool first, int src, int dst)
     {
         if (first)
-            k_grad<true><<<n_tile_blocks, kThreads, 0, s>>>(D, src, dst);
+            k_grad<true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, src, dst);
         else
-            k_grad<false><<<n_tile_blocks, kThreads, 0, s>>>(D, src, dst);
+            k_grad<false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, src, dst);
     }
-    void launch_residual(int gslot)
+    void launch_residual(Part& P, int gslot)
     {
         switch (flux_variant) {
-            case 1: k_residual<4, false><<<res_blocks, kThreads, 0, s>>>(D, gslot, 0); break;
-            case 2: k_residual<3, true><<<res_blocks, kThreads, 0, s>>>(D, gslot, 0); break;
-            case 3: k_residual<4, true><<<res_blocks, kThreads, 0, s>>>(D, gslot, 0); break;
-            default: k_residual<3, false><<<res_blocks, kThreads, 0, s>>>(D, gslot, 0); break;
+            case 1: k_residual<4, false><<<P.res_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
+            case 2: k_residual<3, true><<<P.res_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
+            case 3: k_residual<4, true><<<P.res_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
+            default: k_residual<3, false><<<P.res_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
         }
     }
+    // halo exchanges and the cross-partition reduction
+    void exchange_rec(int slot);
+    void exchange_j(int c);
+    void reduce_rows();
     void build_graphs();
-    void upload_ref4(double4* dst, const double* host);
+    // host <-> device state in reference numbering (all partitions)
+    void upload_state(const double* host, const std::function<double4*(Part&)>& sel);
+    void download_state(double* host, const std::function<const double4*(Part&)>& sel);
     void upload_field(PtRec* dst, int field, const double* host);
     void download_field(double* host, const PtRec* src, int field);
-    void download_ref4(double* host, const double4* src);
+    void set_control(unsigned long long status, int iter);
     std::string message(unsigned long long key, int& point, int& iteration) const;
     void fill_record(kf_iter_record& out, const DevRecord& r, bool accumulate);
+    void require_single(const char* what) const
+    {
+        if (n_rows != 1)
+            throw SolverError(KF_CONFIG, std::string(what) + ": stage hooks need an unpartitioned context");
+    }
 };
 
-Solver::Impl::Impl(const Cloud& c, const kf_config& cf) : cfg(cf)
+Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spec) : cfg(cf)
 {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -207,7 +277,56 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf) : cfg(cf)
         throw SolverError(KF_CONFIG, "cloud needs " + std::to_string(c.n_colors) +
                                          " colours; the device sweep supports at most " +
                                          std::to_string(kMaxColors));
-    pack(c);
+    C = std::max(c.n_colors, 1);
+    if (spec.n_parts < 1) throw SolverError(KF_CONFIG, "n_parts must be >= 1");
+    n_rows = spec.n_parts;
+    transport = spec.n_parts == 1 ? kSingle : (spec.nccl ? kNccl : kInProc);
+    if (transport == kNccl && (spec.rank < 0 || spec.rank >= spec.n_parts))
+        throw SolverError(KF_CONFIG, "rank out of range");
+    {
+        // A/B switch for the residual kernel (register cap x arithmetic)
+        const char* env = std::getenv("KF_FLUX_KERNEL");
+        const std::string v = env ? env : "m4fast";
+        flux_variant = v == "m3" ? 0 : v == "m4" ? 1 : v == "m3fast" ? 2 : 3;
+    }
+    std::vector<double> oty, otx;
+    setup_globals(c, oty, otx);
+
+    const std::vector<uint64_t> code = morton_codes(c);
+    std::vector<int> owner;
+    if (n_rows == 1)
+        owner.assign(c.n, 0);
+    else
+        owner = plan_partition(c, n_rows, spec.mode);
+    double* red_shared = nullptr;
+    const size_t red_len = static_cast<size_t>(W) + kRowStride * static_cast<size_t>(n_rows);
+    if (transport == kInProc) {
+        red_shared = dalloc<double>(red_len, owned);
+        ck(cudaMemsetAsync(red_shared, 0, sizeof(double) * red_len, s), "memset");
+    }
+    std::vector<int> ranks;
+    if (transport == kNccl)
+        ranks.push_back(spec.rank);
+    else
+        for (int r = 0; r < n_rows; ++r) ranks.push_back(r);
+    parts.resize(ranks.size());
+    for (size_t k = 0; k < ranks.size(); ++k) {
+        const LocalLayout L = build_local_layout(c, owner, n_rows, ranks[k], cfg.ordering);
+        parts[k].rank = ranks[k];
+        pack(c, L, code, oty, otx, red_shared, parts[k]);
+    }
+    if (transport == kNccl) {
+        ncclUniqueId id;
+        static_assert(sizeof(id.internal) == KF_NCCL_ID_BYTES, "ncclUniqueId size");
+        std::memcpy(id.internal, spec.nccl_id, KF_NCCL_ID_BYTES);
+        nccl_check(nccl().CommInitRank(&comm, n_rows, id, spec.rank), "ncclCommInitRank");
+        // establish the peer connections eagerly (outside any graph capture)
+        exchange_rec(0);
+        for (int cc = 0; cc < C; ++cc) exchange_j(cc);
+        reduce_rows();
+        ck(cudaStreamSynchronize(s), "nccl warm-up");
+    }
+    ck(cudaStreamSynchronize(s), "pack sync");
     build_graphs();
 }
 
@@ -216,52 +335,128 @@ Solver::Impl::~Impl()
     for (auto& g : graph)
         if (g) cudaGraphExecDestroy(g);
     if (bench_graph) cudaGraphExecDestroy(bench_graph);
+    if (comm) nccl().CommDestroy(comm);
     for (void* p : owned) cudaFree(p);
+    for (auto& P : parts)
+        if (P.hcomp) cudaFreeHost(P.hcomp);
     if (h_status) cudaFreeHost(h_status);
     if (h_iter) cudaFreeHost(h_iter);
     if (s) cudaStreamDestroy(s);
 }
 
-void Solver::Impl::pack(const Cloud& c)
+// Whole-cloud data every partition shares: freestream, initial state, CFL
+// schedule, wall-loop geometry, closed-form counter terms, staging buffers.
+void Solver::Impl::setup_globals(const Cloud& c, std::vector<double>& oty, std::vector<double>& otx)
 {
-    C = std::max(c.n_colors, 1);
-    // ---- renumbering: colour-major, padded to warps, in-colour order
-    std::vector<std::vector<int>> members(C);
-    for (int p = 0; p < n; ++p) members[std::max(c.color[p], 1) - 1].push_back(p);
-    if (cfg.ordering == 1 && n > 0) {
-        const double x0 = *std::min_element(c.x.begin(), c.x.end());
-        const double x1 = *std::max_element(c.x.begin(), c.x.end());
-        const double y0 = *std::min_element(c.y.begin(), c.y.end());
-        const double y1 = *std::max_element(c.y.begin(), c.y.end());
-        const double sx = x1 > x0 ? 4294967295.0 / (x1 - x0) : 0.0;
-        const double sy = y1 > y0 ? 4294967295.0 / (y1 - y0) : 0.0;
-        std::vector<uint64_t> code(n);
-        for (int p = 0; p < n; ++p)
-            code[p] = morton2(static_cast<uint32_t>((c.x[p] - x0) * sx),
-                              static_cast<uint32_t>((c.y[p] - y0) * sy));
-        for (auto& m : members)
-            std::stable_sort(m.begin(), m.end(), [&](int a, int b) { return code[a] < code[b]; });
-    }
-    gs.assign(C, 0);
-    ge.assign(C, 0);
-    perm.clear();
-    std::vector<int> inv(n, -1);
-    for (int g = 0; g < C; ++g) {
-        gs[g] = static_cast<int>(perm.size());
-        for (int p : members[g]) {
-            inv[p] = static_cast<int>(perm.size());
-            perm.push_back(p);
+    // ---- wall loop geometry for compute_forces (driver.cpp:127-167)
+    W = static_cast<int>(c.wall_ids.size());
+    oty.assign(std::max(W, 1), 0.0);
+    otx.assign(std::max(W, 1), 0.0);
+    forces_err = 0;
+    if (W < 3) {
+        forces_err = 1;
+    } else {
+        for (int k = 0; k < W; ++k) {
+            const int a = c.wall_ids[k], b = c.wall_ids[(k + 1) % W];
+            if (std::hypot(c.x[b] - c.x[a], c.y[b] - c.y[a]) > 0.5) forces_err = 2;
         }
-        while (perm.size() % 32) perm.push_back(-1);
-        ge[g] = static_cast<int>(perm.size());
+        double area2 = 0.0;
+        for (int k = 0; k < W; ++k) {
+            const int a = c.wall_ids[k], b = c.wall_ids[(k + 1) % W];
+            area2 += c.x[a] * c.y[b] - c.x[b] * c.y[a];
+        }
+        const double orient = (area2 >= 0.0) ? 1.0 : -1.0;
+        for (int k = 0; k < W; ++k) {
+            const int a = c.wall_ids[k], b = c.wall_ids[(k + 1) % W];
+            const double tx = c.x[b] - c.x[a];
+            const double ty = c.y[b] - c.y[a];
+            oty[k] = orient * ty;
+            otx[k] = orient * (-tx);
+        }
     }
-    if (perm.empty())
-        for (int k = 0; k < 32; ++k) perm.push_back(-1);
-    n_pad = static_cast<int>(perm.size());
+    // ---- evaluation tallies: nonzero split weights of the whole cloud
+    nnz_w = 0;
+    for (int sl = 0; sl < 4; ++sl)
+        for (double w : c.split_w[sl]) nnz_w += w != 0.0;
+
+    // ---- freestream (driver.cpp:12-22) and initial state (driver.cpp:207-208)
+    if (!(cfg.mach_inf > 0.0)) throw SolverError(KF_CONFIG, "freestream Mach must be positive");
+    const double alpha = cfg.aoa_deg * M_PI / 180.0;
+    const double frho = 1.0, fu1 = cfg.mach_inf * std::cos(alpha), fu2 = cfg.mach_inf * std::sin(alpha);
+    const double fp = 1.0 / kGamma;
+    const double frhoe = fp / (kGamma - 1.0) + 0.5 * frho * (fu1 * fu1 + fu2 * fu2);
+    fsU = make_double4(frho, frho * fu1, frho * fu2, frhoe);
+    h_init.assign(4 * static_cast<size_t>(n), 0.0);
+    for (int p = 0; p < n; ++p) {
+        h_init[4 * p] = fsU.x;
+        h_init[4 * p + 1] = fsU.y;
+        h_init[4 * p + 2] = fsU.z;
+        h_init[4 * p + 3] = fsU.w;
+    }
+    if (cfg.bc_mode == 0) {
+        for (int p : c.wall_ids) {
+            double* U = &h_init[4 * p];
+            const double rho = U[0], u1 = U[1] / rho, u2 = U[2] / rho;
+            const double pr = (kGamma - 1.0) * (U[3] - 0.5 * rho * (u1 * u1 + u2 * u2));
+            const double un = u1 * c.nx[p] + u2 * c.ny[p];
+            const double v1 = u1 - un * c.nx[p], v2 = u2 - un * c.ny[p];
+            const double re = pr / (kGamma - 1.0) + 0.5 * rho * (v1 * v1 + v2 * v2);
+            U[0] = rho;
+            U[1] = rho * v1;
+            U[2] = rho * v2;
+            U[3] = re;
+        }
+        // outer points: uniform state, so inflow and outflow both give U_inf
+    }
+    const int cap = std::max(cfg.n_iterations, 1);
+    cfl_h.assign(cap, cfg.cfl);
+    for (int it = 1; it <= cap; ++it) {
+        double cfl = cfg.cfl;
+        if (cfg.cfl_ramp_iters > 0 && it < cfg.cfl_ramp_iters) {  // driver.cpp:222-227
+            const double c0 = (cfg.cfl_start > 0.0) ? cfg.cfl_start : 0.1 * cfg.cfl;
+            cfl = c0 + (cfg.cfl - c0) * it / cfg.cfl_ramp_iters;
+        }
+        cfl_h[it - 1] = cfl;
+    }
+    dstage = dalloc<double4>(std::max(n, 1), owned);
+    dstage1 = dalloc<double>(std::max(n, 1), owned);
+    dstage_i = dalloc<int>(std::max(n, 1), owned);
+    ck(cudaMallocHost(&h_status, sizeof(unsigned long long)), "cudaMallocHost");
+    ck(cudaMallocHost(&h_iter, sizeof(int)), "cudaMallocHost");
+}
+
+void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<uint64_t>& code,
+                        const std::vector<double>& oty, const std::vector<double>& otx,
+                        double* red_shared, Part& P)
+{
+    // ---- renumbering: colour-major, owned then ghosts per colour, padded to warps
+    P.gs = L.gs;
+    P.oe = L.oe;
+    P.ge = L.ge;
+    P.perm = L.perm;
+    P.ghost = L.ghost;
+    P.n_owned = L.n_owned;
+    P.n_pad = static_cast<int>(P.perm.size());
+    const int n_pad = P.n_pad;
     const int n_slices = n_pad / 32;
+    std::vector<int> inv(c.n, -1);
+    P.own_gid.clear();
+    P.loc_gid.clear();
+    std::vector<int> own_loc, loc_loc;
+    for (int pn = 0; pn < n_pad; ++pn) {
+        const int o = P.perm[pn];
+        if (o < 0) continue;
+        inv[o] = pn;
+        P.loc_gid.push_back(o);
+        loc_loc.push_back(pn);
+        if (!P.ghost[pn]) {
+            P.own_gid.push_back(o);
+            own_loc.push_back(pn);
+        }
+    }
 
     // ---- per-point static data
-    std::vector<int> orig(perm);
+    std::vector<int> orig(P.perm);
     std::vector<signed char> kind(n_pad, -1);
     std::vector<double> hmin(n_pad, 0.0);
     std::vector<double4> lsone(n_pad, make_double4(0, 0, 0, 0));
@@ -272,8 +467,9 @@ void Solver::Impl::pack(const Cloud& c)
     for (int sl = 0; sl < n_slices; ++sl) {
         int w = 0;
         for (int l = 0; l < 32; ++l) {
-            const int o = perm[sl * 32 + l];
-            if (o >= 0) w = std::max(w, c.nbr.degree(o));
+            const int pn = sl * 32 + l;
+            const int o = P.perm[pn];
+            if (o >= 0 && !P.ghost[pn]) w = std::max(w, c.nbr.degree(o));
         }
         slice_off[sl + 1] = slice_off[sl] + 32 * w;
     }
@@ -292,13 +488,16 @@ void Solver::Impl::pack(const Cloud& c)
         lsB(n_pad, make_double4(0, 0, 0, 0)), lsD(n_pad, make_double4(1, 1, 1, 1));
     std::vector<double2> lsfd(n_pad, make_double2(1, 1)), xy(n_pad, make_double2(0, 0));
     auto form = [](double A, double B, double Dn, double u, double v) { return (A * u - B * v) / Dn; };
-    nnz_w = 0;
+    std::vector<int> wall_slot_of(c.n, -1);
+    for (int k = 0; k < W && W >= 3; ++k) wall_slot_of[c.wall_ids[k]] = k;
+    P.nnz_w = 0;
     for (int pn = 0; pn < n_pad; ++pn) {
-        const int o = perm[pn];
+        const int o = P.perm[pn];
         if (o < 0) continue;
+        xy[pn] = make_double2(c.x[o], c.y[o]);
+        if (P.ghost[pn]) continue;  // ghosts: coordinates only (gather sources)
         kind[pn] = static_cast<signed char>(c.kind[o]);
         nrm[pn] = make_double2(c.nx[o], c.ny[o]);
-        xy[pn] = make_double2(c.x[o], c.y[o]);
         lsone[pn] = make_double4(c.ls_one[kXpos][o], c.ls_one[kXneg][o], c.ls_one[kYpos][o],
                                  c.ls_one[kYneg][o]);
         lsf[pn] = make_double4(c.coefA[0][o], c.coefB[0][o], c.coefA[1][o], c.coefB[1][o]);
@@ -357,32 +556,33 @@ void Solver::Impl::pack(const Cloud& c)
                 if (f != wd)
                     throw SolverError(KF_RUNTIME, "LS linear form does not reproduce a split weight");
             }
+            if (inv[i] < 0) throw SolverError(KF_RUNTIME, "partition layout misses a neighbour");
             const int kk = k - c.nbr.off[o];
             const size_t e = static_cast<size_t>(slice_off[pn >> 5]) + 32 * kk + (pn & 31);
             e_id[e] = static_cast<unsigned>(inv[i]) | (mask << 28);
-            nnz_w += __builtin_popcount(mask);
+            P.nnz_w += __builtin_popcount(mask);
         }
         hmin[pn] = h;
-        if (c.kind[o] == kOuter) near_int[pn] = best >= 0 ? inv[best] : -1;
+        if (c.kind[o] == kOuter && best >= 0) {
+            // the planner keeps every outer point with its BC source
+            // (partition.cpp), so the source is always a local owned point
+            if (inv[best] < 0 || P.ghost[inv[best]])
+                throw SolverError(KF_RUNTIME, "outer BC source of point " + std::to_string(o) +
+                                                  " is not owned by its partition");
+            near_int[pn] = inv[best];
+        }
+        if (c.kind[o] == kWall) wslot[pn] = wall_slot_of[o];
     }
-    // processing order of the point-parallel kernels: slices sorted by the
-    // Morton code of their first point, so the resident front of a launch is
-    // spatially compact across all colours (L2 reuse of the gathers)
+    // processing order of the point-parallel kernels: owned slices sorted by
+    // the Morton code of their first point, so the resident front of a launch
+    // is spatially compact across all colours (L2 reuse of the gathers)
     std::vector<int> tiles;
     {
-        const double x0 = *std::min_element(c.x.begin(), c.x.end());
-        const double x1 = *std::max_element(c.x.begin(), c.x.end());
-        const double y0 = *std::min_element(c.y.begin(), c.y.end());
-        const double y1 = *std::max_element(c.y.begin(), c.y.end());
-        const double sx = x1 > x0 ? 4294967295.0 / (x1 - x0) : 0.0;
-        const double sy = y1 > y0 ? 4294967295.0 / (y1 - y0) : 0.0;
         std::vector<std::pair<uint64_t, int>> key;
         for (int sl = 0; sl < n_slices; ++sl) {
-            const int o = perm[sl * 32];
-            if (o < 0) continue;
-            key.emplace_back(morton2(static_cast<uint32_t>((c.x[o] - x0) * sx),
-                                     static_cast<uint32_t>((c.y[o] - y0) * sy)),
-                             sl);
+            const int o = P.perm[sl * 32];
+            if (o < 0 || P.ghost[sl * 32]) continue;
+            key.emplace_back(code[o], sl);
         }
         std::stable_sort(key.begin(), key.end());
         for (auto& kv : key) tiles.push_back(kv.second);
@@ -390,72 +590,38 @@ void Solver::Impl::pack(const Cloud& c)
         if (tiles.empty())
             for (int k = 0; k < kThreads / 32; ++k) tiles.push_back(-1);
     }
-    // ---- wall loop geometry for compute_forces (driver.cpp:127-167)
-    const int W = static_cast<int>(c.wall_ids.size());
-    std::vector<double> oty(std::max(W, 1), 0.0), otx(std::max(W, 1), 0.0);
-    forces_err = 0;
-    if (W < 3) {
-        forces_err = 1;
-    } else {
-        for (int k = 0; k < W; ++k) {
-            const int a = c.wall_ids[k], b = c.wall_ids[(k + 1) % W];
-            if (std::hypot(c.x[b] - c.x[a], c.y[b] - c.y[a]) > 0.5) forces_err = 2;
-        }
-        double area2 = 0.0;
-        for (int k = 0; k < W; ++k) {
-            const int a = c.wall_ids[k], b = c.wall_ids[(k + 1) % W];
-            area2 += c.x[a] * c.y[b] - c.x[b] * c.y[a];
-        }
-        const double orient = (area2 >= 0.0) ? 1.0 : -1.0;
-        for (int k = 0; k < W; ++k) {
-            const int a = c.wall_ids[k], b = c.wall_ids[(k + 1) % W];
-            const double tx = c.x[b] - c.x[a];
-            const double ty = c.y[b] - c.y[a];
-            oty[k] = orient * ty;
-            otx[k] = orient * (-tx);
-            wslot[inv[a]] = k;
-        }
-    }
 
-    // ---- freestream (driver.cpp:12-22) and initial state (driver.cpp:207-208)
-    if (!(cfg.mach_inf > 0.0)) throw SolverError(KF_CONFIG, "freestream Mach must be positive");
-    const double alpha = cfg.aoa_deg * M_PI / 180.0;
-    const double frho = 1.0, fu1 = cfg.mach_inf * std::cos(alpha), fu2 = cfg.mach_inf * std::sin(alpha);
-    const double fp = 1.0 / kGamma;
-    const double frhoe = fp / (kGamma - 1.0) + 0.5 * frho * (fu1 * fu1 + fu2 * fu2);
-    fsU = make_double4(frho, frho * fu1, frho * fu2, frhoe);
-    h_init.assign(4 * static_cast<size_t>(n), 0.0);
-    for (int p = 0; p < n; ++p) {
-        h_init[4 * p] = fsU.x;
-        h_init[4 * p + 1] = fsU.y;
-        h_init[4 * p + 2] = fsU.z;
-        h_init[4 * p + 3] = fsU.w;
-    }
-    if (cfg.bc_mode == 0) {
-        for (int p : c.wall_ids) {
-            double* U = &h_init[4 * p];
-            const double rho = U[0], u1 = U[1] / rho, u2 = U[2] / rho;
-            const double pr = (kGamma - 1.0) * (U[3] - 0.5 * rho * (u1 * u1 + u2 * u2));
-            const double un = u1 * c.nx[p] + u2 * c.ny[p];
-            const double v1 = u1 - un * c.nx[p], v2 = u2 - un * c.ny[p];
-            const double re = pr / (kGamma - 1.0) + 0.5 * rho * (v1 * v1 + v2 * v2);
-            U[0] = rho;
-            U[1] = rho * v1;
-            U[2] = rho * v2;
-            U[3] = re;
+    // ---- halo plan (send list colour-major, peer-minor)
+    const int NP = static_cast<int>(L.peers.size());
+    P.peers = L.peers;
+    P.recv_off = L.recv_off;
+    P.recv_cnt = L.recv_cnt;
+    P.send_off.assign(C, std::vector<int>(NP, 0));
+    P.send_cnt.assign(C, std::vector<int>(NP, 0));
+    P.cstart.assign(C + 1, 0);
+    std::vector<int> send_list;
+    for (int cc = 0; cc < C; ++cc) {
+        P.cstart[cc] = static_cast<int>(send_list.size());
+        for (int k = 0; k < NP; ++k) {
+            P.send_off[cc][k] = static_cast<int>(send_list.size());
+            P.send_cnt[cc][k] = static_cast<int>(L.send_idx[k][cc].size());
+            send_list.insert(send_list.end(), L.send_idx[k][cc].begin(), L.send_idx[k][cc].end());
         }
-        // outer points: uniform state, so inflow and outflow both give U_inf
     }
+    P.cstart[C] = static_cast<int>(send_list.size());
+    P.n_send = static_cast<int>(send_list.size());
 
     // ---- device buffers
+    Dev& D = P.D;
     auto up = [&](auto* d, const auto& h) { h2d(d, h.data(), h.size(), s); };
     D.n_pad = n_pad;
     D.n_real = n;
     D.n_colors = C;
     D.n_slices = n_slices;
     for (int g = 0; g < C; ++g) {
-        D.gs[g] = gs[g];
-        D.ge[g] = ge[g];
+        D.gs[g] = P.gs[g];
+        D.oe[g] = P.oe[g];
+        D.ge[g] = P.ge[g];
     }
     int* d_orig = dalloc<int>(n_pad, owned);
     up(d_orig, orig);
@@ -506,18 +672,18 @@ void Solver::Impl::pack(const Cloud& c)
     int* d_tiles = dalloc<int>(tiles.size(), owned);
     up(d_tiles, tiles);
     D.tiles = d_tiles;
-    n_tile_blocks = static_cast<int>(tiles.size()) / (kThreads / 32);
+    P.n_tile_blocks = static_cast<int>(tiles.size()) / (kThreads / 32);
 
     for (int b = 0; b < 2; ++b) {
         D.U[b] = dalloc<double4>(n_pad, owned);
         D.P[b] = dalloc<PtRec>(n_pad, owned);
+        ck(cudaMemsetAsync(D.U[b], 0, sizeof(double4) * n_pad, s), "memset");
     }
     {
         std::vector<PtRec> rec(n_pad);
         for (int pn = 0; pn < n_pad; ++pn) {
             rec[pn] = PtRec{};
-            const int o = perm[pn];
-            rec[pn].xy = o >= 0 ? make_double2(c.x[o], c.y[o]) : make_double2(0, 0);
+            rec[pn].xy = xy[pn];
         }
         up(D.P[0], rec);
         up(D.P[1], rec);
@@ -530,22 +696,17 @@ void Solver::Impl::pack(const Cloud& c)
     D.diag = dalloc<double>(n_pad, owned);
     D.demoted = dalloc<unsigned char>(n_pad, owned);
     ck(cudaMemsetAsync(D.dU, 0, sizeof(double4) * n_pad, s), "memset");
+    ck(cudaMemsetAsync(D.J, 0, sizeof(JRec) * n_pad, s), "memset");
     ck(cudaMemsetAsync(D.jbad, 0, n_pad, s), "memset");
     D.dt_out = nullptr;
     D.S_out = nullptr;
-    D.cp = dalloc<double>(std::max(W, 1), owned);
-    {
-        // A/B switch for the residual kernel (register cap x arithmetic)
-        const char* env = std::getenv("KF_FLUX_KERNEL");
-        const std::string v = env ? env : "m3";
-        flux_variant = v == "m4" ? 1 : v == "m3fast" ? 2 : v == "m4fast" ? 3 : 0;
-    }
-    res_blocks = n_tile_blocks;
-    D.res_part = dalloc<double>(res_blocks, owned);
-    D.cnt_part = dalloc<long long>(res_blocks, owned);
-    D.fo_part = dalloc<int>(res_blocks, owned);
+    P.res_blocks = P.n_tile_blocks;
+    D.res_part = dalloc<double>(P.res_blocks, owned);
+    D.cnt_part = dalloc<long long>(P.res_blocks, owned);
+    D.fo_part = dalloc<int>(P.res_blocks, owned);
     D.fb_part = dalloc<int>(1, owned);
-    D.n_res_blocks = res_blocks;
+    ck(cudaMemsetAsync(D.fb_part, 0, sizeof(int), s), "memset");
+    D.n_res_blocks = P.res_blocks;
     D.status = dalloc<unsigned long long>(1, owned);
     D.iter = dalloc<int>(1, owned);
     D.nrec = dalloc<int>(1, owned);
@@ -555,15 +716,6 @@ void Solver::Impl::pack(const Cloud& c)
     const int cap = std::max(cfg.n_iterations, 1);
     D.rec = dalloc<DevRecord>(cap, owned);
     D.rec_capacity = cap;
-    cfl_h.assign(cap, cfg.cfl);
-    for (int it = 1; it <= cap; ++it) {
-        double cfl = cfg.cfl;
-        if (cfg.cfl_ramp_iters > 0 && it < cfg.cfl_ramp_iters) {  // driver.cpp:222-227
-            const double c0 = (cfg.cfl_start > 0.0) ? cfg.cfl_start : 0.1 * cfg.cfl;
-            cfl = c0 + (cfg.cfl - c0) * it / cfg.cfl_ramp_iters;
-        }
-        cfl_h[it - 1] = cfl;
-    }
     double* d_cfl = dalloc<double>(cap, owned);
     up(d_cfl, cfl_h);
     D.cfl = d_cfl;
@@ -574,8 +726,9 @@ void Solver::Impl::pack(const Cloud& c)
     D.exact = cfg.variant == KF_ANANDH_AD || cfg.variant == KF_MANISH_AD || cfg.variant == KF_EXPLICIT;
     D.bc_mode = cfg.bc_mode;
     D.fsU = fsU;
-    D.fs_p = fp;
-    D.qdyn = 0.5 * frho * cfg.mach_inf * cfg.mach_inf;
+    D.fs_p = 1.0 / kGamma;
+    D.qdyn = 0.5 * 1.0 * cfg.mach_inf * cfg.mach_inf;
+    const double alpha = cfg.aoa_deg * M_PI / 180.0;
     D.ca = std::cos(alpha);
     D.sa = std::sin(alpha);
     D.div_factor = cfg.divergence_factor;
@@ -588,59 +741,215 @@ void Solver::Impl::pack(const Cloud& c)
     up(d_otx, otx);
     D.otx = d_otx;
     D.forces_err = forces_err;
-
-    dstage = dalloc<double4>(std::max(n, 1), owned);
-    dstage1 = dalloc<double>(std::max(n, 1), owned);
-    dstage_i = dalloc<int>(std::max(n, 1), owned);
-    Usnap = dalloc<double4>(n_pad, owned);
-    dUsnap = dalloc<double4>(n_pad, owned);
-    ck(cudaMallocHost(&h_status, sizeof(unsigned long long)), "cudaMallocHost");
-    ck(cudaMallocHost(&h_iter, sizeof(int)), "cudaMallocHost");
+    D.n_rows = n_rows;
+    const size_t red_len = static_cast<size_t>(W) + kRowStride * static_cast<size_t>(n_rows);
+    if (n_rows == 1) {
+        D.cp = dalloc<double>(std::max(W, 1), owned);
+        D.red = nullptr;
+    } else if (red_shared) {
+        P.red_local = P.red = red_shared;
+        D.cp = red_shared;
+        D.red = red_shared;
+    } else {
+        P.red_local = dalloc<double>(red_len, owned);
+        P.red = dalloc<double>(red_len, owned);
+        ck(cudaMemsetAsync(P.red_local, 0, sizeof(double) * red_len, s), "memset");
+        ck(cudaMemsetAsync(P.red, 0, sizeof(double) * red_len, s), "memset");
+        D.cp = P.red_local;
+        D.red = P.red;
+    }
+    // halo staging
+    if (P.n_send) {
+        int* d_send = dalloc<int>(P.n_send, owned);
+        up(d_send, send_list);
+        P.d_send = d_send;
+        P.sendP = dalloc<PtRec>(P.n_send, owned);
+        P.sendJ = dalloc<JRec>(P.n_send, owned);
+        P.sendB = dalloc<unsigned char>(P.n_send, owned);
+    }
+    // compact transfers (multi-process)
+    if (transport == kNccl) {
+        int* d_own = dalloc<int>(own_loc.size(), owned);
+        up(d_own, own_loc);
+        P.d_own = d_own;
+        int* d_loc = dalloc<int>(loc_loc.size(), owned);
+        up(d_loc, loc_loc);
+        P.d_loc = d_loc;
+        P.dcomp = dalloc<double4>(std::max(loc_loc.size(), size_t(1)), owned);
+        ck(cudaMallocHost(&P.hcomp, sizeof(double4) * std::max(loc_loc.size(), size_t(1))), "cudaMallocHost");
+    }
+    P.Usnap = dalloc<double4>(n_pad, owned);
+    P.dUsnap = dalloc<double4>(n_pad, owned);
     ck(cudaStreamSynchronize(s), "pack sync");
+}
+
+void Solver::Impl::mark(const char* name)
+{
+    ++launches;
+    if (prof_ev) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        ck(cudaEventRecord(e, s), "cudaEventRecord");
+        prof_ev->push_back(e);
+        prof_names->push_back(name);
+    }
+}
+
+// Refresh the ghosts of PtRec buffer `slot` (q, qx, qy; all colours).
+void Solver::Impl::exchange_rec(int slot)
+{
+    for (Part& P : parts)
+        if (P.n_send) {
+            k_pack_rec<<<blocks_for(8L * P.n_send, 256), 256, 0, s>>>(P.D.P[slot], P.d_send, P.n_send, P.sendP);
+            mark("halo_pack");
+        }
+    if (transport == kInProc) {
+        for (Part& A : parts)
+            for (size_t k = 0; k < A.peers.size(); ++k) {
+                Part& B = parts[A.peers[k]];
+                const int kb = static_cast<int>(std::find(B.peers.begin(), B.peers.end(), A.rank) - B.peers.begin());
+                for (int cc = 0; cc < C; ++cc) {
+                    const int cnt = A.send_cnt[cc][k];
+                    if (!cnt) continue;
+                    ck(cudaMemcpyAsync(B.D.P[slot] + B.recv_off[kb][cc], A.sendP + A.send_off[cc][k],
+                                       sizeof(PtRec) * cnt, cudaMemcpyDeviceToDevice, s), "halo copy");
+                }
+            }
+    } else if (transport == kNccl) {
+        Part& A = p0();
+        const NcclApi& N = nccl();
+        nccl_check(N.GroupStart(), "ncclGroupStart");
+        for (size_t k = 0; k < A.peers.size(); ++k)
+            for (int cc = 0; cc < C; ++cc) {
+                if (A.send_cnt[cc][k])
+                    nccl_check(N.Send(A.sendP + A.send_off[cc][k], sizeof(PtRec) * A.send_cnt[cc][k], ncclInt8,
+                                      A.peers[k], comm, s), "ncclSend");
+                if (A.recv_cnt[k][cc])
+                    nccl_check(N.Recv(A.D.P[slot] + A.recv_off[k][cc], sizeof(PtRec) * A.recv_cnt[k][cc],
+                                      ncclInt8, A.peers[k], comm, s), "ncclRecv");
+            }
+        nccl_check(N.GroupEnd(), "ncclGroupEnd");
+    }
+}
+
+// Refresh the ghosts of colour c's hoisted JVP records (and validity flags).
+void Solver::Impl::exchange_j(int c)
+{
+    for (Part& P : parts) {
+        const int m = P.cstart[c + 1] - P.cstart[c];
+        if (m) {
+            k_pack_j<<<blocks_for(8L * m, 256), 256, 0, s>>>(P.D.J, P.D.jbad, P.d_send + P.cstart[c], m,
+                                                             P.sendJ + P.cstart[c], P.sendB + P.cstart[c]);
+            mark("halo_pack");
+        }
+    }
+    if (transport == kInProc) {
+        for (Part& A : parts)
+            for (size_t k = 0; k < A.peers.size(); ++k) {
+                const int cnt = A.send_cnt[c][k];
+                if (!cnt) continue;
+                Part& B = parts[A.peers[k]];
+                const int kb = static_cast<int>(std::find(B.peers.begin(), B.peers.end(), A.rank) - B.peers.begin());
+                ck(cudaMemcpyAsync(B.D.J + B.recv_off[kb][c], A.sendJ + A.send_off[c][k], sizeof(JRec) * cnt,
+                                   cudaMemcpyDeviceToDevice, s), "halo copy");
+                ck(cudaMemcpyAsync(B.D.jbad + B.recv_off[kb][c], A.sendB + A.send_off[c][k], cnt,
+                                   cudaMemcpyDeviceToDevice, s), "halo copy");
+            }
+    } else if (transport == kNccl) {
+        Part& A = p0();
+        const NcclApi& N = nccl();
+        nccl_check(N.GroupStart(), "ncclGroupStart");
+        for (size_t k = 0; k < A.peers.size(); ++k) {
+            const int sc = A.send_cnt[c][k], rc = A.recv_cnt[k][c];
+            if (sc) {
+                nccl_check(N.Send(A.sendJ + A.send_off[c][k], sizeof(JRec) * sc, ncclInt8, A.peers[k], comm, s),
+                           "ncclSend");
+                nccl_check(N.Send(A.sendB + A.send_off[c][k], sc, ncclInt8, A.peers[k], comm, s), "ncclSend");
+            }
+            if (rc) {
+                nccl_check(N.Recv(A.D.J + A.recv_off[k][c], sizeof(JRec) * rc, ncclInt8, A.peers[k], comm, s),
+                           "ncclRecv");
+                nccl_check(N.Recv(A.D.jbad + A.recv_off[k][c], rc, ncclInt8, A.peers[k], comm, s), "ncclRecv");
+            }
+        }
+        nccl_check(N.GroupEnd(), "ncclGroupEnd");
+    }
+}
+
+// Combine the partitions' rows and wall Cp (every slot has exactly one
+// writer, so a sum with the other ranks' zeros is exact and every rank ends
+// with the same buffer).
+void Solver::Impl::reduce_rows()
+{
+    if (transport != kNccl) return;  // in-process partitions share one buffer
+    Part& A = p0();
+    const size_t len = static_cast<size_t>(W) + kRowStride * static_cast<size_t>(n_rows);
+    nccl_check(nccl().AllReduce(A.red_local, A.red, len, ncclFloat64, ncclSum, comm, s), "ncclAllReduce");
 }
 
 void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
 {
     const int T = kThreads;
+    const bool halo = multi();
     launches = 0;
-    auto mark = [&](const char* name) {
-        ++launches;
-        if (prof_ev) {
-            cudaEvent_t e;
-            ck(cudaEventCreate(&e), "cudaEventCreate");
-            ck(cudaEventRecord(e, s), "cudaEventRecord");
-            prof_ev->push_back(e);
-            prof_names->push_back(name);
+    if (with_q)
+        for (Part& P : parts) {
+            k_q_from_u<<<blocks_for(P.n_pad, 256), 256, 0, s>>>(P.D, cb, 0);
+            mark("q_from_u");
         }
-    };
-    if (with_q) {
-        k_q_from_u<<<blocks_for(n_pad, 256), 256, 0, s>>>(D, cb, 0);
-        mark("q_from_u");
+    if (halo) exchange_rec(0);  // ghost q of this iteration
+    for (Part& P : parts) {
+        launch_grad(P, true, 0, 0);
+        mark("grad_pass1");
     }
-    launch_grad(true, 0, 0);
-    mark("grad_pass1");
+    if (halo) exchange_rec(0);
     int slot = 0;
     for (int pass = 2; pass <= cfg.n_inner; ++pass) {
-        launch_grad(false, slot, slot ^ 1);
+        for (Part& P : parts) {
+            launch_grad(P, false, slot, slot ^ 1);
+            mark("grad_passk");
+        }
         slot ^= 1;
-        mark("grad_passk");
+        if (halo) exchange_rec(slot);
     }
-    launch_residual(slot);
-    mark("flux_residual");
-    if (D.implicit) {
+    for (Part& P : parts) {
+        launch_residual(P, slot);
+        mark("flux_residual");
+    }
+    if (parts[0].D.implicit) {
         for (int c = 0; c < C; ++c) {
-            k_forward<<<blocks_for(ge[c] - gs[c], T), T, 0, s>>>(D, cb, c, cfl_override);
-            mark("lusgs_forward");
+            for (Part& P : parts) {
+                k_forward<<<blocks_for(P.oe[c] - P.gs[c], T), T, 0, s>>>(P.D, cb, c, cfl_override);
+                mark("lusgs_forward");
+            }
+            if (halo && C > 1) exchange_j(c);
         }
         for (int c = C - 2; c >= 0; --c) {
-            k_backward<<<blocks_for(ge[c] - gs[c], T), T, 0, s>>>(D, cb, c);
-            mark("lusgs_backward");
+            for (Part& P : parts) {
+                k_backward<<<blocks_for(P.oe[c] - P.gs[c], T), T, 0, s>>>(P.D, cb, c);
+                mark("lusgs_backward");
+            }
+            if (halo && c > 0) exchange_j(c);
         }
     }
-    k_update<<<blocks_for(n_pad, 256), 256, 0, s>>>(D, cb, cfl_override);
-    mark("update_bc_q");
-    k_finalize<<<1, 1024, 0, s>>>(D);
-    mark("finalize");
+    for (Part& P : parts) {
+        k_update<<<blocks_for(P.n_pad, 256), 256, 0, s>>>(P.D, cb, cfl_override);
+        mark("update_bc_q");
+    }
+    if (halo) {
+        for (Part& P : parts) {
+            k_partials<<<1, 1024, 0, s>>>(P.D, P.red_local, P.rank);
+            mark("partials");
+        }
+        reduce_rows();
+        for (Part& P : parts) {
+            k_finalize<true><<<1, 1024, 0, s>>>(P.D);
+            mark("finalize");
+        }
+    } else {
+        k_finalize<false><<<1, 1024, 0, s>>>(parts[0].D);
+        mark("finalize");
+    }
 }
 
 void Solver::Impl::build_graphs()
@@ -656,28 +965,64 @@ void Solver::Impl::build_graphs()
     }
 }
 
-void Solver::Impl::upload_ref4(double4* dst, const double* host)
+void Solver::Impl::upload_state(const double* host, const std::function<double4*(Part&)>& sel)
 {
-    h2d(dstage, reinterpret_cast<const double4*>(host), n, s);
-    k_to_dev<<<blocks_for(n_pad, 256), 256, 0, s>>>(dst, dstage, D.orig, n_pad);
+    if (transport != kNccl) {
+        h2d(dstage, reinterpret_cast<const double4*>(host), n, s);
+        for (Part& P : parts)
+            k_to_dev<<<blocks_for(P.n_pad, 256), 256, 0, s>>>(sel(P), dstage, P.D.orig, P.n_pad);
+        return;
+    }
+    // this rank's points only: host gather -> pinned -> device scatter
+    Part& P = p0();
+    ck(cudaStreamSynchronize(s), "sync");  // hcomp may still feed an earlier copy
+    const double4* h = reinterpret_cast<const double4*>(host);
+    const int m = static_cast<int>(P.loc_gid.size());
+    for (int j = 0; j < m; ++j) P.hcomp[j] = h[P.loc_gid[j]];
+    h2d(P.dcomp, P.hcomp, m, s);
+    double4* dst = sel(P);
+    ck(cudaMemsetAsync(dst, 0, sizeof(double4) * P.n_pad, s), "memset");
+    if (m) k_scatter_local<<<blocks_for(m, 256), 256, 0, s>>>(dst, P.dcomp, P.d_loc, m);
+}
+
+void Solver::Impl::download_state(double* host, const std::function<const double4*(Part&)>& sel)
+{
+    if (transport != kNccl) {
+        for (Part& P : parts)
+            k_to_ref<<<blocks_for(P.n_pad, 256), 256, 0, s>>>(dstage, sel(P), P.D.orig, P.D.kind, P.n_pad);
+        d2h(reinterpret_cast<double4*>(host), dstage, n, s);
+        return;
+    }
+    // this rank's owned points only (other entries of `host` are untouched)
+    Part& P = p0();
+    const int m = static_cast<int>(P.own_gid.size());
+    if (m) k_gather_local<<<blocks_for(m, 256), 256, 0, s>>>(P.dcomp, sel(P), P.d_own, m);
+    d2h(P.hcomp, P.dcomp, m, s);
+    ck(cudaStreamSynchronize(s), "sync");
+    double4* h = reinterpret_cast<double4*>(host);
+    for (int j = 0; j < m; ++j) h[P.own_gid[j]] = P.hcomp[j];
 }
 
 void Solver::Impl::upload_field(PtRec* dst, int field, const double* host)
 {
     h2d(dstage, reinterpret_cast<const double4*>(host), n, s);
-    k_ref_to_rec<<<blocks_for(n_pad, 256), 256, 0, s>>>(dst, field, dstage, D.orig, n_pad);
+    k_ref_to_rec<<<blocks_for(p0().n_pad, 256), 256, 0, s>>>(dst, field, dstage, p0().D.orig, p0().n_pad);
 }
 
 void Solver::Impl::download_field(double* host, const PtRec* src, int field)
 {
-    k_rec_to_ref<<<blocks_for(n_pad, 256), 256, 0, s>>>(dstage, src, field, D.orig, n_pad);
+    k_rec_to_ref<<<blocks_for(p0().n_pad, 256), 256, 0, s>>>(dstage, src, field, p0().D.orig, p0().n_pad);
     d2h(reinterpret_cast<double4*>(host), dstage, n, s);
 }
 
-void Solver::Impl::download_ref4(double* host, const double4* src)
+void Solver::Impl::set_control(unsigned long long status, int iter)
 {
-    k_to_ref<<<blocks_for(n_pad, 256), 256, 0, s>>>(dstage, src, D.orig, n_pad);
-    d2h(reinterpret_cast<double4*>(host), dstage, n, s);
+    for (Part& P : parts) {
+        ck(cudaMemcpyAsync(P.D.status, &status, sizeof status, cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaMemcpyAsync(P.D.iter, &iter, sizeof iter, cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaMemcpyAsync(P.D.nrec, &iter, sizeof iter, cudaMemcpyHostToDevice, s), "H2D");
+    }
+    ck(cudaStreamSynchronize(s), "set_control");  // sources are host stack values
 }
 
 std::string Solver::Impl::message(unsigned long long key, int& point, int& iteration) const
@@ -717,6 +1062,7 @@ void Solver::Impl::fill_record(kf_iter_record& o, const DevRecord& r, bool accum
     uint64_t sw[5] = {0, 0, 0, 0, 0};
     it[0] += r.res_flux;
     it[2] += r.res_flux;
+    const Dev& D = parts[0].D;
     if (D.implicit) {
         if (D.exact) {
             sw[3] = nnz_w;
@@ -744,7 +1090,10 @@ void Solver::Impl::fill_record(kf_iter_record& o, const DevRecord& r, bool accum
 
 // ---------------------------------------------------------------- Solver
 
-Solver::Solver(const Cloud& cloud, const kf_config& cfg) : impl_(new Impl(cloud, cfg)) {}
+Solver::Solver(const Cloud& cloud, const kf_config& cfg, const PartitionSpec& spec)
+    : impl_(new Impl(cloud, cfg, spec))
+{
+}
 Solver::~Solver() = default;
 
 void* Solver::stream() const { return impl_->s; }
@@ -752,7 +1101,14 @@ int Solver::launches_per_iteration() const
 {
     // one kf_iterate_async step: the captured iteration, plus restart and q in
     // benchmark mode
-    return impl_->bench ? impl_->launches_bench + 1 : impl_->launches;
+    return impl_->bench ? impl_->launches_bench + static_cast<int>(impl_->parts.size()) : impl_->launches;
+}
+int Solver::n_parts() const { return impl_->n_rows; }
+int Solver::owned_points() const
+{
+    int m = 0;
+    for (const Part& P : impl_->parts) m += P.n_owned;
+    return m;
 }
 
 void Solver::reset()
@@ -760,19 +1116,20 @@ void Solver::reset()
     Impl& I = *impl_;
     I.bench = 0;
     I.cur = 0;
-    I.upload_ref4(I.D.U[0], I.h_init.data());
-    ck(cudaMemsetAsync(I.D.dU, 0, sizeof(double4) * I.n_pad, I.s), "memset");
-    const unsigned long long nokey = kNoKey;
+    I.upload_state(I.h_init.data(), [](Part& P) { return P.D.U[0]; });
     const int zero = 0;
     const double m1 = -1.0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.diverged, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.fb_part, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.res0, &m1, sizeof m1, cudaMemcpyHostToDevice, I.s), "H2D");
-    k_q_from_u<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, 0, 1);
-    k_stamp<<<1, 1, 0, I.s>>>(I.D);
+    for (Part& P : I.parts) {
+        ck(cudaMemsetAsync(P.D.dU, 0, sizeof(double4) * P.n_pad, I.s), "memset");
+        ck(cudaMemcpyAsync(P.D.diverged, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+        ck(cudaMemcpyAsync(P.D.fb_part, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+        ck(cudaMemcpyAsync(P.D.res0, &m1, sizeof m1, cudaMemcpyHostToDevice, I.s), "H2D");
+    }
+    I.set_control(kNoKey, 0);
+    for (Part& P : I.parts) {
+        k_q_from_u<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(P.D, 0, 1);
+        k_stamp<<<1, 1, 0, I.s>>>(P.D);
+    }
     for (auto& v : I.total_counters) v = 0;
     ck(cudaStreamSynchronize(I.s), "reset");
     ck(cudaGetLastError(), "reset launch");
@@ -782,18 +1139,16 @@ void Solver::set_state(const double* U, const double* dU_prev)
 {
     Impl& I = *impl_;
     I.cur = 0;
-    I.upload_ref4(I.D.U[0], U);
+    I.upload_state(U, [](Part& P) { return P.D.U[0]; });
     if (dU_prev)
-        I.upload_ref4(I.D.dU, dU_prev);
+        I.upload_state(dU_prev, [](Part& P) { return P.D.dU; });
     else
-        ck(cudaMemsetAsync(I.D.dU, 0, sizeof(double4) * I.n_pad, I.s), "memset");
-    const unsigned long long nokey = kNoKey;
-    const int zero = 0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    k_q_from_u<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, 0, 1);
-    k_stamp<<<1, 1, 0, I.s>>>(I.D);
+        for (Part& P : I.parts) ck(cudaMemsetAsync(P.D.dU, 0, sizeof(double4) * P.n_pad, I.s), "memset");
+    I.set_control(kNoKey, 0);
+    for (Part& P : I.parts) {
+        k_q_from_u<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(P.D, 0, 1);
+        k_stamp<<<1, 1, 0, I.s>>>(P.D);
+    }
     ck(cudaStreamSynchronize(I.s), "set_state");
 }
 
@@ -801,10 +1156,11 @@ void Solver::get_state(double* U, double* dU_prev)
 {
     Impl& I = *impl_;
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.download_ref4(U, I.D.U[I.cur]);
+    const int cb = I.cur;
+    I.download_state(U, [cb](Part& P) { return static_cast<const double4*>(P.D.U[cb]); });
     if (dU_prev) {
         ck(cudaStreamSynchronize(I.s), "sync");
-        I.download_ref4(dU_prev, I.D.dU);
+        I.download_state(dU_prev, [](Part& P) { return static_cast<const double4*>(P.D.dU); });
     }
     ck(cudaStreamSynchronize(I.s), "get_state");
 }
@@ -814,8 +1170,8 @@ void Solver::iterate_async(int n)
     Impl& I = *impl_;
     for (int k = 0; k < n; ++k) {
         if (I.bench) {
-            k_bench_restart<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, I.Usnap, I.dUsnap,
-                                                                      I.snap_iter);
+            for (Part& P : I.parts)
+                k_bench_restart<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(P.D, P.Usnap, P.dUsnap, I.snap_iter);
             if (I.cfg.use_graph && I.bench_graph) {
                 ck(cudaGraphLaunch(I.bench_graph, I.s), "graph launch");
             } else {
@@ -852,11 +1208,13 @@ void Solver::bench_mode(int mode)
         I.launches = saved;
     }
     // snapshot the current state (I.cur) and the iteration counter
-    ck(cudaMemcpyAsync(I.Usnap, I.D.U[I.cur], sizeof(double4) * I.n_pad, cudaMemcpyDeviceToDevice, I.s), "D2D");
-    ck(cudaMemcpyAsync(I.dUsnap, I.D.dU, sizeof(double4) * I.n_pad, cudaMemcpyDeviceToDevice, I.s), "D2D");
-    ck(cudaMemcpyAsync(I.h_iter, I.D.nrec, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
+    for (Part& P : I.parts) {
+        ck(cudaMemcpyAsync(P.Usnap, P.D.U[I.cur], sizeof(double4) * P.n_pad, cudaMemcpyDeviceToDevice, I.s), "D2D");
+        ck(cudaMemcpyAsync(P.dUsnap, P.D.dU, sizeof(double4) * P.n_pad, cudaMemcpyDeviceToDevice, I.s), "D2D");
+    }
+    ck(cudaMemcpyAsync(I.h_iter, I.p0().D.nrec, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.snap_iter = std::min(*I.h_iter, I.D.rec_capacity - 1);
+    I.snap_iter = std::min(*I.h_iter, I.p0().D.rec_capacity - 1);
     I.bench = 1;
     if (I.cfg.use_graph && !I.bench_graph) {
         cudaGraph_t g;
@@ -873,15 +1231,16 @@ int Solver::sync_records(kf_iter_record* records, int capacity, int* n_done, std
                          int& point, int& iteration)
 {
     Impl& I = *impl_;
-    ck(cudaMemcpyAsync(I.h_status, I.D.status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, I.s), "D2H");
-    ck(cudaMemcpyAsync(I.h_iter, I.D.nrec, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
+    const Dev& D = I.p0().D;
+    ck(cudaMemcpyAsync(I.h_status, D.status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, I.s), "D2H");
+    ck(cudaMemcpyAsync(I.h_iter, D.nrec, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
     ck(cudaStreamSynchronize(I.s), "sync");
-    int nd = std::min(*I.h_iter, I.D.rec_capacity);
+    int nd = std::min(*I.h_iter, D.rec_capacity);
     if (n_done) *n_done = nd;
     if (records && capacity > 0) {
         const int m = std::min(nd, capacity);
         I.rec_h.resize(std::max(m, 1));
-        d2h(I.rec_h.data(), I.D.rec, m, I.s);
+        d2h(I.rec_h.data(), D.rec, m, I.s);
         ck(cudaStreamSynchronize(I.s), "sync");
         for (auto& v : I.total_counters) v = 0;
         for (int k = 0; k < m; ++k) I.fill_record(records[k], I.rec_h[k], true);
@@ -906,11 +1265,14 @@ int Solver::run(kf_iter_record* records, int* n_done, double* final_state, doubl
     const int total = I.cfg.n_iterations;
     int issued = 0;
     unsigned long long key = kNoKey;
+    // every partition holds the same (globally reduced) status after each
+    // k_finalize, so all ranks leave this loop after the same chunk
     while (issued < total) {
         const int m = std::min(chunk, total - issued);
         iterate_async(m);
         issued += m;
-        ck(cudaMemcpyAsync(I.h_status, I.D.status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, I.s), "D2H");
+        ck(cudaMemcpyAsync(I.h_status, I.p0().D.status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, I.s),
+           "D2H");
         ck(cudaStreamSynchronize(I.s), "run sync");
         key = *I.h_status;
         if (key != kNoKey) break;
@@ -923,7 +1285,7 @@ int Solver::run(kf_iter_record* records, int* n_done, double* final_state, doubl
     if (n_done) *n_done = done;
     key = *I.h_status;
     int diverged = 0;
-    ck(cudaMemcpy(&diverged, I.D.diverged, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(&diverged, I.p0().D.diverged, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
     if (key != kNoKey && key_stage(key) == ST_Q && key_reason(key) == RS_STOP && diverged) {
         code = KF_DIVERGED;
         reason = "residual diverged";
@@ -931,28 +1293,32 @@ int Solver::run(kf_iter_record* records, int* n_done, double* final_state, doubl
         iteration = done;
     }
     if (final_state) {
+        auto ubuf = [](int b) {
+            return [b](Part& P) { return static_cast<const double4*>(P.D.U[b]); };
+        };
         // Which buffer holds the reference's final state (driver.cpp:255-262,280)
         const int after_last = done % 2;  // state after BCs of the last completed iteration
         if (key == kNoKey || (key_stage(key) == ST_Q && key_reason(key) == RS_STOP)) {
-            I.download_ref4(final_state, I.D.U[after_last]);
+            I.download_state(final_state, ubuf(after_last));
         } else {
             const int st = key_stage(key);
             const int failed_it = static_cast<int>(key_iter(key));
             const int cur_buf = (failed_it - 1) % 2;
             if (st == ST_SWEEP0 + 2 * I.C) {
                 // exception after U += dU (implicit) / partial explicit update
-                std::vector<double> U(4 * static_cast<size_t>(I.n)), dU(4 * static_cast<size_t>(I.n));
-                I.download_ref4(U.data(), I.D.U[cur_buf]);
-                if (I.D.implicit) {
-                    I.download_ref4(dU.data(), I.D.dU);
+                const size_t m = 4 * static_cast<size_t>(I.n);
+                std::vector<double> U(final_state, final_state + m), dU(m, 0.0);
+                I.download_state(U.data(), ubuf(cur_buf));
+                if (I.p0().D.implicit) {
+                    I.download_state(dU.data(), [](Part& P) { return static_cast<const double4*>(P.D.dU); });
                     ck(cudaStreamSynchronize(I.s), "sync");
                     for (size_t k = 0; k < U.size(); ++k) U[k] += dU[k];
                 } else {
                     // explicit_update modifies points 0..P in index order before
                     // throwing at P (driver.cpp:101-110); k_update left the raw
                     // (pre-BC) update of every point in dUs.
-                    std::vector<double> Vraw(4 * static_cast<size_t>(I.n));
-                    I.download_ref4(Vraw.data(), I.D.dUs);
+                    std::vector<double> Vraw(U);
+                    I.download_state(Vraw.data(), [](Part& P) { return static_cast<const double4*>(P.D.dUs); });
                     ck(cudaStreamSynchronize(I.s), "sync");
                     for (int p = 0; p <= point && p < I.n; ++p)
                         for (int j = 0; j < 4; ++j) U[4 * p + j] = Vraw[4 * p + j];
@@ -960,9 +1326,9 @@ int Solver::run(kf_iter_record* records, int* n_done, double* final_state, doubl
                 ck(cudaStreamSynchronize(I.s), "sync");
                 std::memcpy(final_state, U.data(), U.size() * sizeof(double));
             } else if (st > ST_SWEEP0 + 2 * I.C) {
-                I.download_ref4(final_state, I.D.U[failed_it % 2]);
+                I.download_state(final_state, ubuf(failed_it % 2));
             } else {
-                I.download_ref4(final_state, I.D.U[cur_buf]);
+                I.download_state(final_state, ubuf(cur_buf));
             }
         }
         ck(cudaStreamSynchronize(I.s), "sync");
@@ -976,22 +1342,25 @@ int Solver::step_host(const double* U_in, const double* dU_in, double* U_out, do
 {
     Impl& I = *impl_;
     // H2D of this step's inputs, one iteration, D2H of the result.
-    I.upload_ref4(I.D.U[0], U_in);
-    I.upload_ref4(I.D.dU, dU_in);
+    I.upload_state(U_in, [](Part& P) { return P.D.U[0]; });
+    I.upload_state(dU_in, [](Part& P) { return P.D.dU; });
     const unsigned long long nokey = kNoKey;
     const int zero = 0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    for (Part& P : I.parts) {
+        ck(cudaMemcpyAsync(P.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
+        ck(cudaMemcpyAsync(P.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+        ck(cudaMemcpyAsync(P.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
+    }
     if (I.cfg.use_graph && I.bench_graph)
         ck(cudaGraphLaunch(I.bench_graph, I.s), "graph launch");
     else
         I.enqueue_iteration(0, 0.0, true);
-    I.download_ref4(U_out, I.D.U[1]);
-    if (dU_out) I.download_ref4(dU_out, I.D.dU);
+    I.download_state(U_out, [](Part& P) { return static_cast<const double4*>(P.D.U[1]); });
+    if (dU_out) I.download_state(dU_out, [](Part& P) { return static_cast<const double4*>(P.D.dU); });
     DevRecord r;
-    d2h(&r, I.D.rec, 1, I.s);
-    ck(cudaMemcpyAsync(I.h_status, I.D.status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, I.s), "D2H");
+    d2h(&r, I.p0().D.rec, 1, I.s);
+    ck(cudaMemcpyAsync(I.h_status, I.p0().D.status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, I.s),
+       "D2H");
     ck(cudaStreamSynchronize(I.s), "step sync");
     I.cur = 1;
     if (rec) I.fill_record(*rec, r, false);
@@ -1007,15 +1376,13 @@ int Solver::step_host(const double* U_in, const double* dU_in, double* U_out, do
 int Solver::stage_q(const double* U, double* q, std::string& reason, int& point)
 {
     Impl& I = *impl_;
-    I.upload_ref4(I.D.U[0], U);
-    const unsigned long long nokey = kNoKey;
-    const int zero = 0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    k_q_from_u<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, 0, 1);
-    I.download_field(q, I.D.P[0], 0);
-    d2h(I.h_status, I.D.status, 1, I.s);
+    I.require_single("stage_q");
+    Part& Q = I.p0();
+    I.upload_state(U, [](Part& P) { return P.D.U[0]; });
+    I.set_control(kNoKey, 0);
+    k_q_from_u<<<blocks_for(Q.n_pad, 256), 256, 0, I.s>>>(Q.D, 0, 1);
+    I.download_field(q, Q.D.P[0], 0);
+    d2h(I.h_status, Q.D.status, 1, I.s);
     ck(cudaStreamSynchronize(I.s), "stage_q");
     if (*I.h_status != kNoKey) {
         int it;
@@ -1028,22 +1395,20 @@ int Solver::stage_q(const double* U, double* q, std::string& reason, int& point)
 int Solver::stage_grads(const double* q, double* qx, double* qy)
 {
     Impl& I = *impl_;
-    const unsigned long long nokey = kNoKey;
-    const int zero = 0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    I.upload_field(I.D.P[0], 0, q);
-    I.upload_field(I.D.P[1], 0, q);
-    I.launch_grad(true, 0, 0);
+    I.require_single("stage_grads");
+    Part& Q = I.p0();
+    I.set_control(kNoKey, 0);
+    I.upload_field(Q.D.P[0], 0, q);
+    I.upload_field(Q.D.P[1], 0, q);
+    I.launch_grad(Q, true, 0, 0);
     int slot = 0;
     for (int pass = 2; pass <= I.cfg.n_inner; ++pass) {
-        I.launch_grad(false, slot, slot ^ 1);
+        I.launch_grad(Q, false, slot, slot ^ 1);
         slot ^= 1;
     }
-    I.download_field(qx, I.D.P[slot], 1);
+    I.download_field(qx, Q.D.P[slot], 1);
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.download_field(qy, I.D.P[slot], 2);
+    I.download_field(qy, Q.D.P[slot], 2);
     ck(cudaStreamSynchronize(I.s), "stage_grads");
     return KF_OK;
 }
@@ -1052,24 +1417,22 @@ int Solver::stage_residual(const double* q, const double* qx, const double* qy, 
                            int* demoted, std::string& reason, int& point)
 {
     Impl& I = *impl_;
-    const unsigned long long nokey = kNoKey;
-    const int zero = 0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    I.upload_field(I.D.P[0], 0, q);
+    I.require_single("stage_residual");
+    Part& Q = I.p0();
+    I.set_control(kNoKey, 0);
+    I.upload_field(Q.D.P[0], 0, q);
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.upload_field(I.D.P[0], 1, qx);
+    I.upload_field(Q.D.P[0], 1, qx);
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.upload_field(I.D.P[0], 2, qy);
-    I.launch_residual(0);
-    I.download_ref4(R, I.D.R);
+    I.upload_field(Q.D.P[0], 2, qy);
+    I.launch_residual(Q, 0);
+    I.download_state(R, [](Part& P) { return static_cast<const double4*>(P.D.R); });
     ck(cudaStreamSynchronize(I.s), "sync");
     if (demoted) {
-        k_to_ref_u8<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.dstage_i, I.D.demoted, I.D.orig, I.n_pad);
+        k_to_ref_u8<<<blocks_for(Q.n_pad, 256), 256, 0, I.s>>>(I.dstage_i, Q.D.demoted, Q.D.orig, Q.n_pad);
         d2h(demoted, I.dstage_i, I.n, I.s);
     }
-    d2h(I.h_status, I.D.status, 1, I.s);
+    d2h(I.h_status, Q.D.status, 1, I.s);
     ck(cudaStreamSynchronize(I.s), "stage_residual");
     if (*I.h_status != kNoKey) {
         int it;
@@ -1084,46 +1447,44 @@ int Solver::stage_lusgs(const double* U, const double* R, const double* dU_prev,
                         std::string& reason, int& point)
 {
     Impl& I = *impl_;
-    if (!I.D.implicit) throw SolverError(KF_CONFIG, "lusgs_step: explicit variant");
-    const unsigned long long nokey = kNoKey;
-    const int zero = 0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    I.upload_ref4(I.D.U[0], U);
+    I.require_single("stage_lusgs");
+    Part& Q = I.p0();
+    if (!Q.D.implicit) throw SolverError(KF_CONFIG, "lusgs_step: explicit variant");
+    I.set_control(kNoKey, 0);
+    I.upload_state(U, [](Part& P) { return P.D.U[0]; });
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.upload_ref4(I.D.R, R);
+    I.upload_state(R, [](Part& P) { return P.D.R; });
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.upload_ref4(I.D.dU, dU_prev);
-    Dev D = I.D;
+    I.upload_state(dU_prev, [](Part& P) { return P.D.dU; });
+    Dev D = Q.D;
     double* d_dt = nullptr;
     double4* d_S = nullptr;
-    ck(cudaMalloc(&d_dt, sizeof(double) * I.n_pad), "cudaMalloc");
-    ck(cudaMalloc(&d_S, sizeof(double4) * I.n_pad), "cudaMalloc");
+    ck(cudaMalloc(&d_dt, sizeof(double) * Q.n_pad), "cudaMalloc");
+    ck(cudaMalloc(&d_S, sizeof(double4) * Q.n_pad), "cudaMalloc");
     D.dt_out = d_dt;
     D.S_out = d_S;
     for (int c = 0; c < I.C; ++c)
-        k_forward<<<blocks_for(I.ge[c] - I.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c, cfl);
+        k_forward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c, cfl);
     for (int c = I.C - 2; c >= 0; --c)
-        k_backward<<<blocks_for(I.ge[c] - I.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c);
+        k_backward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c);
     ck(cudaGetLastError(), "lusgs launch");
     auto grab1 = [&](double* h, const double* d) {
         if (!h) return;
-        k_to_ref1<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.dstage1, d, I.D.orig, I.n_pad);
+        k_to_ref1<<<blocks_for(Q.n_pad, 256), 256, 0, I.s>>>(I.dstage1, d, Q.D.orig, Q.n_pad);
         d2h(h, I.dstage1, I.n, I.s);
         ck(cudaStreamSynchronize(I.s), "sync");
     };
     auto grab4 = [&](double* h, const double4* d) {
         if (!h) return;
-        I.download_ref4(h, d);
+        I.download_state(h, [d](Part&) { return d; });
         ck(cudaStreamSynchronize(I.s), "sync");
     };
     grab1(dt, d_dt);
-    grab1(diag, I.D.diag);
-    if (S && I.D.with_s) grab4(S, d_S);
-    grab4(dUs, I.D.dUs);
-    grab4(dU, I.D.dU);
-    d2h(I.h_status, I.D.status, 1, I.s);
+    grab1(diag, Q.D.diag);
+    if (S && Q.D.with_s) grab4(S, d_S);
+    grab4(dUs, Q.D.dUs);
+    grab4(dU, Q.D.dU);
+    d2h(I.h_status, Q.D.status, 1, I.s);
     ck(cudaStreamSynchronize(I.s), "stage_lusgs");
     cudaFree(d_dt);
     cudaFree(d_S);
@@ -1139,18 +1500,16 @@ int Solver::stage_update(const double* U, const double* dU, double* U_out, std::
                          int& point)
 {
     Impl& I = *impl_;
-    if (!I.D.implicit) throw SolverError(KF_CONFIG, "stage_update: implicit variants only");
-    const unsigned long long nokey = kNoKey;
-    const int zero = 0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    I.upload_ref4(I.D.U[0], U);
+    I.require_single("stage_update");
+    Part& Q = I.p0();
+    if (!Q.D.implicit) throw SolverError(KF_CONFIG, "stage_update: implicit variants only");
+    I.set_control(kNoKey, 0);
+    I.upload_state(U, [](Part& P) { return P.D.U[0]; });
     ck(cudaStreamSynchronize(I.s), "sync");
-    I.upload_ref4(I.D.dU, dU);
-    k_update<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, 0, I.cfg.cfl);
-    I.download_ref4(U_out, I.D.U[1]);
-    d2h(I.h_status, I.D.status, 1, I.s);
+    I.upload_state(dU, [](Part& P) { return P.D.dU; });
+    k_update<<<blocks_for(Q.n_pad, 256), 256, 0, I.s>>>(Q.D, 0, I.cfg.cfl);
+    I.download_state(U_out, [](Part& P) { return static_cast<const double4*>(P.D.U[1]); });
+    d2h(I.h_status, Q.D.status, 1, I.s);
     ck(cudaStreamSynchronize(I.s), "stage_update");
     const unsigned long long key = *I.h_status;
     if (key != kNoKey && key_stage(key) != ST_Q) {
@@ -1164,20 +1523,18 @@ int Solver::stage_update(const double* U, const double* dU, double* U_out, std::
 int Solver::stage_forces(const double* U, double* cl, double* cd, std::string& reason)
 {
     Impl& I = *impl_;
-    const unsigned long long nokey = kNoKey;
-    const int zero = 0;
-    ck(cudaMemcpyAsync(I.D.status, &nokey, sizeof nokey, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemcpyAsync(I.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
-    ck(cudaMemsetAsync(I.D.res_part, 0, sizeof(double) * I.res_blocks, I.s), "memset");
-    ck(cudaMemsetAsync(I.D.cnt_part, 0, sizeof(long long) * I.res_blocks, I.s), "memset");
-    ck(cudaMemsetAsync(I.D.fo_part, 0, sizeof(int) * I.res_blocks, I.s), "memset");
-    I.upload_ref4(I.D.U[1], U);
-    k_cp<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, 1);
-    k_finalize<<<1, 1024, 0, I.s>>>(I.D);
+    I.require_single("stage_forces");
+    Part& Q = I.p0();
+    I.set_control(kNoKey, 0);
+    ck(cudaMemsetAsync(Q.D.res_part, 0, sizeof(double) * Q.res_blocks, I.s), "memset");
+    ck(cudaMemsetAsync(Q.D.cnt_part, 0, sizeof(long long) * Q.res_blocks, I.s), "memset");
+    ck(cudaMemsetAsync(Q.D.fo_part, 0, sizeof(int) * Q.res_blocks, I.s), "memset");
+    I.upload_state(U, [](Part& P) { return P.D.U[1]; });
+    k_cp<<<blocks_for(Q.n_pad, 256), 256, 0, I.s>>>(Q.D, 1);
+    k_finalize<false><<<1, 1024, 0, I.s>>>(Q.D);
     DevRecord r;
-    d2h(&r, I.D.rec, 1, I.s);
-    d2h(I.h_status, I.D.status, 1, I.s);
+    d2h(&r, Q.D.rec, 1, I.s);
+    d2h(I.h_status, Q.D.status, 1, I.s);
     ck(cudaStreamSynchronize(I.s), "stage_forces");
     const unsigned long long key = *I.h_status;
     if (key != kNoKey && !(key_stage(key) == ST_Q && key_reason(key) == RS_STOP)) {
@@ -1240,9 +1597,12 @@ int device_count()
     return n;
 }
 
-}  // namespace kfb
-
-namespace kfb {
+void nccl_unique_id(void* out)
+{
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, id.internal, KF_NCCL_ID_BYTES);
+}
 
 void Solver::profile_kernels(int reps, std::vector<std::string>& names, std::vector<float>& ms)
 {
@@ -1253,7 +1613,8 @@ void Solver::profile_kernels(int reps, std::vector<std::string>& names, std::vec
     std::vector<std::string> nm;
     for (int r = 0; r < reps; ++r) {
         if (I.bench)
-            k_bench_restart<<<blocks_for(I.n_pad, 256), 256, 0, I.s>>>(I.D, I.Usnap, I.dUsnap, I.snap_iter);
+            for (Part& P : I.parts)
+                k_bench_restart<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(P.D, P.Usnap, P.dUsnap, I.snap_iter);
         ck(cudaEventCreate(&starts[r]), "cudaEventCreate");
         ck(cudaEventRecord(starts[r], I.s), "cudaEventRecord");
         nm.clear();
