@@ -146,6 +146,11 @@ int blocks_for(long n, int t) { return static_cast<int>((n + t - 1) / t); }
 
 enum Transport : int { kSingle = 0, kInProc = 1, kNccl = 2 };
 
+// staged records per tile (own points + stencil neighbours); 767 x 14 doubles
+// = 86 KB of shared memory at most (NACA O-grids need <= 372)
+constexpr int kHaloCap = 767;
+constexpr size_t kMaxTileSmem = 200 * 1024;
+
 }  // namespace
 
 // One partition's device layout and buffers.
@@ -158,6 +163,8 @@ struct Part {
     std::vector<int> own_gid, loc_gid;   // owned / owned+ghost global ids (compact transfers)
     Dev D{};
     int n_tile_blocks = 0, res_blocks = 0;
+    int n_tiles = 0, nh_cap = 1, w_max = 0;
+    size_t tile_smem = 0, tile_smem1 = 0;  // dynamic SMEM of the staged kernels (pass >= 2 / residual, pass 1)
     long long nnz_w = 0;
     // halo plan: peers (ascending rank); recv ranges [peer][colour] in local
     // numbering; send list colour-major, peer-minor: entries of (c, k) at
@@ -229,8 +236,18 @@ struct Solver::Impl {
     void setup_globals(const Cloud& c, std::vector<double>& oty, std::vector<double>& otx);
     void enqueue_iteration(int cur_buf, double cfl_override, bool with_q);
     void mark(const char* name);
+    // neighbour gathers of the gradient / residual kernels: 1 SMEM-staged
+    // tiles (default), 0 global-gather sliced ELL (A/B reference)
+    int gather = 1;
     void launch_grad(Part& P, bool first, int src, int dst)
     {
+        if (gather) {
+            if (first)
+                k_grad_t<true><<<P.n_tiles, kThreads, P.tile_smem1, s>>>(P.D, src, dst);
+            else
+                k_grad_t<false><<<P.n_tiles, kThreads, P.tile_smem, s>>>(P.D, src, dst);
+            return;
+        }
         if (first)
             k_grad<true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, src, dst);
         else
@@ -238,14 +255,34 @@ struct Solver::Impl {
     }
     void launch_residual(Part& P, int gslot)
     {
+        if (gather) {
+            const size_t sm = P.tile_smem;
+            switch (flux_variant) {
+                case 1: k_residual_t<4, false><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
+                case 2: k_residual_t<3, true><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
+                case 3: k_residual_t<4, true><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
+                default: k_residual_t<3, false><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
+            }
+            return;
+        }
         switch (flux_variant) {
-            case 1: k_residual<4, false><<<P.res_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
-            case 2: k_residual<3, true><<<P.res_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
-            case 3: k_residual<4, true><<<P.res_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
-            default: k_residual<3, false><<<P.res_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
+            case 1: k_residual<4, false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
+            case 2: k_residual<3, true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
+            case 3: k_residual<4, true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
+            default: k_residual<3, false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
         }
     }
     // halo exchanges and the cross-partition reduction
+    struct Msg {
+        int part, peer;
+        bool send;
+        void* buf;
+        size_t bytes;
+    };
+    std::vector<Msg> msgs;
+    void post(Part& P, bool send, int peer, void* buf, size_t bytes);
+    void begin_exchange();
+    void flush_exchange();
     void exchange_rec(int slot);
     void exchange_j(int c);
     void reduce_rows();
@@ -288,6 +325,9 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         const char* env = std::getenv("KF_FLUX_KERNEL");
         const std::string v = env ? env : "m4fast";
         flux_variant = v == "m3" ? 0 : v == "m4" ? 1 : v == "m3fast" ? 2 : 3;
+        // A/B switch for the neighbour gathers of the gradient/residual kernels
+        const char* g = std::getenv("KF_GATHER");
+        gather = (g && std::string(g) == "ell") ? 0 : 1;
     }
     std::vector<double> oty, otx;
     setup_globals(c, oty, otx);
@@ -488,6 +528,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         lsB(n_pad, make_double4(0, 0, 0, 0)), lsD(n_pad, make_double4(1, 1, 1, 1));
     std::vector<double2> lsfd(n_pad, make_double2(1, 1)), xy(n_pad, make_double2(0, 0));
     auto form = [](double A, double B, double Dn, double u, double v) { return (A * u - B * v) / Dn; };
+    std::vector<unsigned char> emask(c.nbr.idx.size(), 0);  // split mask per nbr entry
     std::vector<int> wall_slot_of(c.n, -1);
     for (int k = 0; k < W && W >= 3; ++k) wall_slot_of[c.wall_ids[k]] = k;
     P.nnz_w = 0;
@@ -560,6 +601,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             const int kk = k - c.nbr.off[o];
             const size_t e = static_cast<size_t>(slice_off[pn >> 5]) + 32 * kk + (pn & 31);
             e_id[e] = static_cast<unsigned>(inv[i]) | (mask << 28);
+            emask[k] = static_cast<unsigned char>(mask);
             P.nnz_w += __builtin_popcount(mask);
         }
         hmin[pn] = h;
@@ -590,6 +632,109 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         if (tiles.empty())
             for (int k = 0; k < kThreads / 32; ++k) tiles.push_back(-1);
     }
+
+    // ---- SMEM-staged tiles of the gradient / residual kernels: owned points
+    // in Morton order, greedily cut into tiles of <= kThreads points whose
+    // staged set (own points + their stencil neighbours) stays <= kHaloCap
+    std::vector<int> tpts, thoff(1, 0), thalo, teoff(1, 0);
+    std::vector<unsigned short> tell;
+    std::vector<double4> tlsf, tlsA, tlsB, tlsD;
+    std::vector<double2> tlsfd;
+    int nh_max = 1;
+    {
+        int halo_cap = kHaloCap;
+        if (const char* e = std::getenv("KF_TILE_CAP")) halo_cap = std::max(64, std::min(kHaloCap, std::atoi(e)));
+        std::vector<int> own;
+        for (int pn = 0; pn < n_pad; ++pn)
+            if (P.perm[pn] >= 0 && !P.ghost[pn]) own.push_back(pn);
+        std::stable_sort(own.begin(), own.end(), [&](int a, int b) { return code[P.perm[a]] < code[P.perm[b]]; });
+        std::vector<int> stamp(n_pad, -1), sstamp(n_pad, -1), slot(n_pad, -1);
+        size_t next = 0;
+        int tcount = 0;
+        std::vector<int> pts, added;
+        while (next < own.size()) {
+            pts.clear();
+            int hcount = 0;
+            while (next < own.size() && static_cast<int>(pts.size()) < kThreads) {
+                const int pn = own[next];
+                const int o = P.perm[pn];
+                added.clear();
+                auto touch = [&](int id) {
+                    if (stamp[id] != tcount) {
+                        stamp[id] = tcount;
+                        added.push_back(id);
+                    }
+                };
+                touch(pn);
+                for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) touch(inv[c.nbr.idx[k]]);
+                if (hcount + static_cast<int>(added.size()) > halo_cap && !pts.empty()) {
+                    for (int id : added) stamp[id] = -1;
+                    break;
+                }
+                hcount += static_cast<int>(added.size());
+                pts.push_back(pn);
+                ++next;
+            }
+            if (hcount > 4095) throw SolverError(KF_CONFIG, "stencil too large for a 12-bit tile slot");
+            // slots: own points first (lane order), then neighbours by first use
+            int ns = 0;
+            auto slot_of = [&](int id) {
+                if (sstamp[id] != tcount) {
+                    sstamp[id] = tcount;
+                    slot[id] = ns++;
+                    thalo.push_back(id);
+                }
+                return slot[id];
+            };
+            for (int pn : pts) slot_of(pn);
+            int W = 0;
+            for (int pn : pts) W = std::max(W, c.nbr.degree(P.perm[pn]));
+            P.w_max = std::max(P.w_max, W);
+            std::vector<unsigned short> ent(static_cast<size_t>(W) * kThreads, 0);
+            for (int t = 0; t < static_cast<int>(pts.size()); ++t) {
+                const int o = P.perm[pts[t]];
+                const int deg = c.nbr.degree(o);
+                for (int kk = 0; kk < W; ++kk) {
+                    unsigned e = static_cast<unsigned>(t);  // padding: self, no split
+                    if (kk < deg) {
+                        const int k = c.nbr.off[o] + kk;
+                        e = static_cast<unsigned>(slot_of(inv[c.nbr.idx[k]])) | (unsigned(emask[k]) << 12);
+                    }
+                    ent[static_cast<size_t>(kk) * kThreads + t] = static_cast<unsigned short>(e);
+                }
+            }
+            tell.insert(tell.end(), ent.begin(), ent.end());
+            teoff.push_back(static_cast<int>(tell.size()));
+            thoff.push_back(static_cast<int>(thalo.size()));
+            nh_max = std::max(nh_max, ns);
+            for (int t = 0; t < kThreads; ++t) {
+                const bool real = t < static_cast<int>(pts.size());
+                const int pn = real ? pts[t] : 0;
+                tpts.push_back(real ? pn : -1);
+                tlsf.push_back(real ? lsf[pn] : make_double4(0, 0, 0, 0));
+                tlsfd.push_back(real ? lsfd[pn] : make_double2(1, 1));
+                tlsA.push_back(real ? lsA[pn] : make_double4(0, 0, 0, 0));
+                tlsB.push_back(real ? lsB[pn] : make_double4(0, 0, 0, 0));
+                tlsD.push_back(real ? lsD[pn] : make_double4(1, 1, 1, 1));
+            }
+            ++tcount;
+        }
+        if (tcount == 0) {  // empty partition: one idle tile
+            tpts.assign(kThreads, -1);
+            tlsf.assign(kThreads, make_double4(0, 0, 0, 0));
+            tlsfd.assign(kThreads, make_double2(1, 1));
+            tlsA.assign(kThreads, make_double4(0, 0, 0, 0));
+            tlsB = tlsA;
+            tlsD.assign(kThreads, make_double4(1, 1, 1, 1));
+            thoff.push_back(0);
+            teoff.push_back(0);
+            thalo.push_back(0);
+            tell.push_back(0);
+            tcount = 1;
+        }
+        P.n_tiles = tcount;
+    }
+    P.nh_cap = nh_max | 1;  // odd: SoA field rows start on different banks
 
     // ---- halo plan (send list colour-major, peer-minor)
     const int NP = static_cast<int>(L.peers.size());
@@ -673,6 +818,41 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     up(d_tiles, tiles);
     D.tiles = d_tiles;
     P.n_tile_blocks = static_cast<int>(tiles.size()) / (kThreads / 32);
+    {
+        auto upi = [&](const std::vector<int>& h) {
+            int* d = dalloc<int>(h.size(), owned);
+            up(d, h);
+            return static_cast<const int*>(d);
+        };
+        D.n_tiles = P.n_tiles;
+        D.nh_cap = P.nh_cap;
+        D.w_max = P.w_max;
+        D.t_pts = upi(tpts);
+        D.t_hoff = upi(thoff);
+        D.t_halo = upi(thalo);
+        D.t_eoff = upi(teoff);
+        unsigned short* d_ell = dalloc<unsigned short>(tell.size(), owned);
+        up(d_ell, tell);
+        D.t_ell = d_ell;
+        D.t_lsf = up4(tlsf);
+        D.t_lsfd = up2(tlsfd);
+        D.t_lsA = up4(tlsA);
+        D.t_lsB = up4(tlsB);
+        D.t_lsD = up4(tlsD);
+        const size_t ent_bytes = static_cast<size_t>(P.w_max) * kThreads * sizeof(unsigned short);
+        P.tile_smem = static_cast<size_t>(kTileUnits) * P.nh_cap * sizeof(double2) + ent_bytes;
+        P.tile_smem1 = static_cast<size_t>(3) * P.nh_cap * sizeof(double2) + ent_bytes;
+        if (P.tile_smem > kMaxTileSmem) throw SolverError(KF_CONFIG, "tile staging exceeds shared memory");
+        // the attribute is per function (process-wide): never lower it below
+        // what another context or partition launches with
+        const int sm = static_cast<int>(std::max<size_t>(P.tile_smem, kMaxTileSmem));
+        ck(cudaFuncSetAttribute(k_grad_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_grad_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+    }
 
     for (int b = 0; b < 2; ++b) {
         D.U[b] = dalloc<double4>(n_pad, owned);
@@ -700,13 +880,13 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     ck(cudaMemsetAsync(D.jbad, 0, n_pad, s), "memset");
     D.dt_out = nullptr;
     D.S_out = nullptr;
-    P.res_blocks = P.n_tile_blocks;
+    P.res_blocks = std::max(P.n_tile_blocks, P.n_tiles);
     D.res_part = dalloc<double>(P.res_blocks, owned);
     D.cnt_part = dalloc<long long>(P.res_blocks, owned);
     D.fo_part = dalloc<int>(P.res_blocks, owned);
     D.fb_part = dalloc<int>(1, owned);
     ck(cudaMemsetAsync(D.fb_part, 0, sizeof(int), s), "memset");
-    D.n_res_blocks = P.res_blocks;
+    D.n_res_blocks = gather ? P.n_tiles : P.n_tile_blocks;  // blocks of the residual launch
     D.status = dalloc<unsigned long long>(1, owned);
     D.iter = dalloc<int>(1, owned);
     D.nrec = dalloc<int>(1, owned);
@@ -786,6 +966,8 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
 void Solver::Impl::mark(const char* name)
 {
     ++launches;
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) throw SolverError(KF_CUDA, std::string(name) + " launch: " + cudaGetErrorString(e));
     if (prof_ev) {
         cudaEvent_t e;
         ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -793,6 +975,61 @@ void Solver::Impl::mark(const char* name)
         prof_ev->push_back(e);
         prof_names->push_back(name);
     }
+}
+
+// Halo messages. Every partition held by this context posts its sends and
+// receives in the same order the NCCL transport issues them (per peer, per
+// colour); flush() either hands them to NCCL as one group, or -- in-process
+// -- pairs each send of (a -> b) with the next receive of (b <- a) in posting
+// order (NCCL's point-to-point matching rule) and issues the device copy,
+// refusing any size mismatch. Both transports therefore move exactly the same
+// message list, and the single-GPU tests exercise the NCCL schedule.
+void Solver::Impl::post(Part& P, bool send, int peer, void* buf, size_t bytes)
+{
+    if (!bytes) return;
+    if (transport == kNccl) {
+        const NcclApi& N = nccl();
+        if (send)
+            nccl_check(N.Send(buf, bytes, ncclInt8, peer, comm, s), "ncclSend");
+        else
+            nccl_check(N.Recv(buf, bytes, ncclInt8, peer, comm, s), "ncclRecv");
+        return;
+    }
+    msgs.push_back(Msg{P.rank, peer, send, buf, bytes});
+}
+
+void Solver::Impl::begin_exchange()
+{
+    msgs.clear();
+    if (transport == kNccl) nccl_check(nccl().GroupStart(), "ncclGroupStart");
+}
+
+void Solver::Impl::flush_exchange()
+{
+    if (transport == kNccl) {
+        nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+        return;
+    }
+    std::vector<char> used(msgs.size(), 0);
+    for (size_t i = 0; i < msgs.size(); ++i) {
+        const Msg& snd = msgs[i];
+        if (!snd.send) continue;
+        size_t j = 0;
+        for (; j < msgs.size(); ++j)
+            if (!used[j] && !msgs[j].send && msgs[j].part == snd.peer && msgs[j].peer == snd.part) break;
+        if (j == msgs.size())
+            throw SolverError(KF_RUNTIME, "halo: send " + std::to_string(snd.part) + " -> " +
+                                              std::to_string(snd.peer) + " has no matching receive");
+        if (msgs[j].bytes != snd.bytes)
+            throw SolverError(KF_RUNTIME, "halo: message size mismatch " + std::to_string(snd.part) + " -> " +
+                                              std::to_string(snd.peer));
+        used[j] = 1;
+        ck(cudaMemcpyAsync(msgs[j].buf, snd.buf, snd.bytes, cudaMemcpyDeviceToDevice, s), "halo copy");
+    }
+    for (size_t j = 0; j < msgs.size(); ++j)
+        if (!msgs[j].send && !used[j])
+            throw SolverError(KF_RUNTIME, "halo: receive without a matching send");
+    msgs.clear();
 }
 
 // Refresh the ghosts of PtRec buffer `slot` (q, qx, qy; all colours).
@@ -803,33 +1040,14 @@ void Solver::Impl::exchange_rec(int slot)
             k_pack_rec<<<blocks_for(8L * P.n_send, 256), 256, 0, s>>>(P.D.P[slot], P.d_send, P.n_send, P.sendP);
             mark("halo_pack");
         }
-    if (transport == kInProc) {
-        for (Part& A : parts)
-            for (size_t k = 0; k < A.peers.size(); ++k) {
-                Part& B = parts[A.peers[k]];
-                const int kb = static_cast<int>(std::find(B.peers.begin(), B.peers.end(), A.rank) - B.peers.begin());
-                for (int cc = 0; cc < C; ++cc) {
-                    const int cnt = A.send_cnt[cc][k];
-                    if (!cnt) continue;
-                    ck(cudaMemcpyAsync(B.D.P[slot] + B.recv_off[kb][cc], A.sendP + A.send_off[cc][k],
-                                       sizeof(PtRec) * cnt, cudaMemcpyDeviceToDevice, s), "halo copy");
-                }
-            }
-    } else if (transport == kNccl) {
-        Part& A = p0();
-        const NcclApi& N = nccl();
-        nccl_check(N.GroupStart(), "ncclGroupStart");
-        for (size_t k = 0; k < A.peers.size(); ++k)
+    begin_exchange();
+    for (Part& P : parts)
+        for (size_t k = 0; k < P.peers.size(); ++k)
             for (int cc = 0; cc < C; ++cc) {
-                if (A.send_cnt[cc][k])
-                    nccl_check(N.Send(A.sendP + A.send_off[cc][k], sizeof(PtRec) * A.send_cnt[cc][k], ncclInt8,
-                                      A.peers[k], comm, s), "ncclSend");
-                if (A.recv_cnt[k][cc])
-                    nccl_check(N.Recv(A.D.P[slot] + A.recv_off[k][cc], sizeof(PtRec) * A.recv_cnt[k][cc],
-                                      ncclInt8, A.peers[k], comm, s), "ncclRecv");
+                post(P, true, P.peers[k], P.sendP + P.send_off[cc][k], sizeof(PtRec) * P.send_cnt[cc][k]);
+                post(P, false, P.peers[k], P.D.P[slot] + P.recv_off[k][cc], sizeof(PtRec) * P.recv_cnt[k][cc]);
             }
-        nccl_check(N.GroupEnd(), "ncclGroupEnd");
-    }
+    flush_exchange();
 }
 
 // Refresh the ghosts of colour c's hoisted JVP records (and validity flags).
@@ -843,37 +1061,16 @@ void Solver::Impl::exchange_j(int c)
             mark("halo_pack");
         }
     }
-    if (transport == kInProc) {
-        for (Part& A : parts)
-            for (size_t k = 0; k < A.peers.size(); ++k) {
-                const int cnt = A.send_cnt[c][k];
-                if (!cnt) continue;
-                Part& B = parts[A.peers[k]];
-                const int kb = static_cast<int>(std::find(B.peers.begin(), B.peers.end(), A.rank) - B.peers.begin());
-                ck(cudaMemcpyAsync(B.D.J + B.recv_off[kb][c], A.sendJ + A.send_off[c][k], sizeof(JRec) * cnt,
-                                   cudaMemcpyDeviceToDevice, s), "halo copy");
-                ck(cudaMemcpyAsync(B.D.jbad + B.recv_off[kb][c], A.sendB + A.send_off[c][k], cnt,
-                                   cudaMemcpyDeviceToDevice, s), "halo copy");
-            }
-    } else if (transport == kNccl) {
-        Part& A = p0();
-        const NcclApi& N = nccl();
-        nccl_check(N.GroupStart(), "ncclGroupStart");
-        for (size_t k = 0; k < A.peers.size(); ++k) {
-            const int sc = A.send_cnt[c][k], rc = A.recv_cnt[k][c];
-            if (sc) {
-                nccl_check(N.Send(A.sendJ + A.send_off[c][k], sizeof(JRec) * sc, ncclInt8, A.peers[k], comm, s),
-                           "ncclSend");
-                nccl_check(N.Send(A.sendB + A.send_off[c][k], sc, ncclInt8, A.peers[k], comm, s), "ncclSend");
-            }
-            if (rc) {
-                nccl_check(N.Recv(A.D.J + A.recv_off[k][c], sizeof(JRec) * rc, ncclInt8, A.peers[k], comm, s),
-                           "ncclRecv");
-                nccl_check(N.Recv(A.D.jbad + A.recv_off[k][c], rc, ncclInt8, A.peers[k], comm, s), "ncclRecv");
-            }
+    begin_exchange();
+    for (Part& P : parts)
+        for (size_t k = 0; k < P.peers.size(); ++k) {
+            const int sc = P.send_cnt[c][k], rc = P.recv_cnt[k][c];
+            post(P, true, P.peers[k], P.sendJ + P.send_off[c][k], sizeof(JRec) * sc);
+            post(P, true, P.peers[k], P.sendB + P.send_off[c][k], sc);
+            post(P, false, P.peers[k], P.D.J + P.recv_off[k][c], sizeof(JRec) * rc);
+            post(P, false, P.peers[k], P.D.jbad + P.recv_off[k][c], rc);
         }
-        nccl_check(N.GroupEnd(), "ncclGroupEnd");
-    }
+    flush_exchange();
 }
 
 // Combine the partitions' rows and wall Cp (every slot has exactly one
