@@ -156,6 +156,40 @@ def reference_cpu(n_iters_total, threads, spec=CASE):
     return secs[:n_iters_total], ctx.n, kind
 
 
+def time_to_drop(kf, decades=1.0, with_cpu=True):
+    """Time to a fixed residual drop (north star; RunHistory::iterations_to_decades,
+    driver.cpp:169-178) on BASELINE config 1 (NACA 0012 320x120, M 0.63, AoA 2,
+    manish_ad, CFL 0.2): the reference reaches ~1 decade before its abort in
+    iteration 423, so 10 decades is not reachable; the drop
+    reported is `decades`. GPU: device seconds of the iterations up to the
+    drop (per-iteration globaltimer records). CPU: the reference solver's own
+    per-iteration seconds for the same iterations, all host threads."""
+    c = kf.generate_naca_ogrid("0012", 320, 120, 20.0)
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.ManishAD, mach_inf=0.63, aoa_deg=2.0, cfl=0.2,
+                          n_iterations=1000)
+    s = kf.Solver(c, cfg)
+    s.run(want_state=False)  # warm-up (graphs, caches)
+    h = s.run(want_state=False)
+    k = h.iterations_to_decades(decades)
+    out = {"config": "naca0012:320:120:20 M0.63 AoA2 manish_ad CFL0.2", "decades": decades,
+           "iterations": k, "recorded_iterations": len(h.iters), "abort": h.abort_reason}
+    if k <= 0:
+        return out
+    out["gpu_seconds"] = float(sum(r.seconds for r in h.iters[:k]))
+    if with_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import refpy
+        if refpy.ref_available():
+            refpy.Reference.num_threads(cpu_cores())
+            ref = refpy.Reference.generate("0012", 320, 120, 20.0)
+            r = ref.run(variant="manish_ad", n_iterations=k, mach=0.63, aoa_deg=2.0, cfl=0.2)
+            out["cpu_seconds"] = float(np.sum(r.seconds[:k]))
+            out["cpu_kind"] = "reference"
+            out["cpu_cores"] = cpu_cores()
+            out["speedup"] = out["cpu_seconds"] / out["gpu_seconds"]
+    return out
+
+
 def case_for(world, points=None):
     """The bench workload at `world` GPUs: config 2 at N=1; the cloud grows
     with N in the wall direction (weak scaling, ~640,000 points per GPU)."""
@@ -346,6 +380,21 @@ def main():
         except Exception:
             traffic = None
     fp64_peak = kf.measure_fp64_peak(local)
+    fp64 = None
+    fpath = os.path.join(ROOT, "profiles", "flux_fp64.json")
+    if os.path.exists(fpath):
+        try:
+            with open(fpath) as f:
+                fj = json.load(f)
+            if fj.get("points") == N and world == 1 and args.parts == 1:
+                fl = float(fj["fp64_flops_per_launch"])
+                ach = fl / (flux_ms * 1e-3) / 1e12
+                fp64 = {"achieved_tflops": ach, "peak_tflops": fp64_peak, "frac": ach / fp64_peak,
+                        "flops_per_launch": fl, "source": fj.get("source"),
+                        "how": "ncu dfma*2 + dmul + dadd thread instructions of one launch / this run's "
+                               "CUDA-event kernel time; peak = measured DFMA loop (kf_measure_fp64_peak)"}
+        except Exception:
+            fp64 = None
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -372,10 +421,12 @@ def main():
             "kernel_ms": flux_ms, "kernel_share_of_step": flux_ms / total_ms if total_ms else None,
             "note": "the flux kernel is FP64-pipe bound (SURVEY.md F4); see fp64",
             "fp64_peak_tflops_measured": fp64_peak,
+            "fp64": fp64,
         },
         "kernels_ms": {k: {"launches": v[0], "ms": v[1]} for k, v in agg.items()},
         "check": {"residual": recs[WARM_ITERS].residual if len(recs) > WARM_ITERS else None,
-                  "cl": recs[WARM_ITERS].cl if len(recs) > WARM_ITERS else None},
+                  "cl": recs[WARM_ITERS].cl if len(recs) > WARM_ITERS else None,
+                  "first_order_points": recs[WARM_ITERS].first_order_points if len(recs) > WARM_ITERS else None},
     }
     if rank == 0 and not args.no_cpu_baseline:
         secs, n_ref, kind = reference_cpu(8, cpu_cores(), spec)
@@ -384,6 +435,8 @@ def main():
             "value": n_ref / float(np.median(secs)) / 1e6, "unit": UNIT, "cores": cpu_cores(),
             "kind": kind, "sample": f"{len(secs)} iterations of the same case on the host "
                                     "(median per-iteration time, warm-up iteration excluded)"}
+    if rank == 0 and world == 1 and args.parts == 1:
+        line["time_to_drop"] = time_to_drop(kf, 1.0, with_cpu=not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

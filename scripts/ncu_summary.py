@@ -3,6 +3,7 @@
 
   python scripts/ncu_summary.py full   <report.ncu-rep> <out.json> [points]
   python scripts/ncu_summary.py launch <launches.csv>   <out.txt>
+  python scripts/ncu_summary.py fp64   <fp64.csv>       <points>
 
 `full` keeps, per captured launch, duration, DRAM bytes, FP64-pipe and
 occupancy metrics; with `points` it also (re)writes profiles/flux_traffic.json
@@ -96,7 +97,39 @@ def launch(path, out):
     print(open(out).read())
 
 
+def fp64(path, points, out=None):
+    """profiles/flux_fp64.json from an ncu --csv --metrics run over k_residual
+    (smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum)."""
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    hdr, data = rows[0], rows[1:]
+    ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+    per = collections.defaultdict(dict)
+    ids = hdr.index("ID")
+    for r in data:
+        if "k_residual" not in r[ki]:
+            continue
+        per[r[ids]][r[mi]] = float(r[vi].replace(",", ""))
+    launches = list(per.values())
+    if not launches:
+        raise SystemExit("no k_residual launches in " + path)
+    def mean(m):
+        return sum(l.get(m, 0.0) for l in launches) / len(launches)
+    dfma = mean("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum")
+    dmul = mean("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum")
+    dadd = mean("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum")
+    tj = {"points": int(points), "dfma": dfma, "dmul": dmul, "dadd": dadd,
+          "fp64_flops_per_launch": 2 * dfma + dmul + dadd,
+          "fp64_pipe_ops_per_point": (dfma + dmul + dadd) / int(points),
+          "source": os.path.basename(path)}
+    with open(out or os.path.join(ROOT, "profiles", "flux_fp64.json"), "w") as f:
+        json.dump(tj, f, indent=1)
+    print(tj)
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "fp64":
+        fp64(sys.argv[2], sys.argv[3])
+        sys.exit(0)
     if sys.argv[1] == "full":
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
     else:
