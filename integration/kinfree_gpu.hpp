@@ -16,6 +16,12 @@
  * the caller's colouring (plan.color_of), so the LU-SGS ordering is the
  * caller's. The evaluation tallies are added to the process-global
  * flux_counters() (counters.hpp:58) so run_case's rdp_report.csv is unchanged.
+ *
+ * n_parts > 1 runs the domain-decomposed solver (kf_create_partitioned): the
+ * cloud is cut into n_parts angular wedges held on `device`, ghosts refreshed
+ * between dependent stages; the RunHistory is the same contract (states are
+ * bitwise the one-partition states, the residual sum is reassociated).
+ * The one-process-per-GPU form is run_fixed_point_rank() below.
  */
 #ifndef KINFREE_GPU_HPP
 #define KINFREE_GPU_HPP
@@ -49,11 +55,12 @@ inline void throw_status(const kf_status& s)
 
 }  // namespace detail
 
-inline RunHistory run_fixed_point(const PointCloud& cloud, const LsCoefficients& ls,
-                                  const SweepPlan& plan, const SolverConfig& config,
-                                  std::vector<Vec4>* final_state, int device = 0)
+namespace detail {
+
+inline RunHistory run_impl(const PointCloud& cloud, const SweepPlan& plan, const SolverConfig& config,
+                           std::vector<Vec4>* final_state, int device, int n_parts, int rank,
+                           const unsigned char* nccl_id)
 {
-    (void)ls;  // rebuilt on the library side, bit-identically
     const int n = cloud.n();
     std::vector<int> kind(n), off(n + 1, 0), ids;
     for (int p = 0; p < n; ++p) {
@@ -61,14 +68,14 @@ inline RunHistory run_fixed_point(const PointCloud& cloud, const LsCoefficients&
         off[p + 1] = off[p] + static_cast<int>(cloud.nbr[p].size());
         ids.insert(ids.end(), cloud.nbr[p].begin(), cloud.nbr[p].end());
     }
-    detail::CloudHandle ch;
+    CloudHandle ch;
     kf_status s = kf_cloud_from_arrays(n, cloud.x.data(), cloud.y.data(), kind.data(),
                                        cloud.normal_x.data(), cloud.normal_y.data(), off.data(),
                                        ids.data(), &ch.c);
-    if (s.code) detail::throw_status(s);
+    if (s.code) throw_status(s);
     if (static_cast<int>(plan.color_of.size()) == n) {
         s = kf_cloud_set_colors(ch.c, plan.color_of.data());
-        if (s.code) detail::throw_status(s);
+        if (s.code) throw_status(s);
     }
 
     kf_config cfg;
@@ -86,16 +93,24 @@ inline RunHistory run_fixed_point(const PointCloud& cloud, const LsCoefficients&
     cfg.divergence_factor = config.divergence_factor;
     cfg.device = device;
 
-    detail::CtxHandle ctx;
-    s = kf_create(ch.c, &cfg, &ctx.c);
-    if (s.code) detail::throw_status(s);  // same precondition errors as driver.cpp:194-201
+    CtxHandle ctx;
+    if (nccl_id)
+        s = kf_create_rank(ch.c, &cfg, n_parts, rank, KF_PART_ANGULAR, nccl_id, &ctx.c);
+    else if (n_parts > 1)
+        s = kf_create_partitioned(ch.c, &cfg, n_parts, KF_PART_ANGULAR, &ctx.c);
+    else
+        s = kf_create(ch.c, &cfg, &ctx.c);
+    if (s.code) throw_status(s);  // same precondition errors as driver.cpp:194-201
 
     std::vector<kf_iter_record> rec(std::max(config.n_iterations, 1));
     std::vector<double> state(final_state ? 4 * static_cast<size_t>(n) : 0);
+    if (final_state && static_cast<int>(final_state->size()) == n)  // rank runs keep non-owned entries
+        for (int p = 0; p < n; ++p)
+            for (int j = 0; j < 4; ++j) state[4 * static_cast<size_t>(p) + j] = (*final_state)[p][j];
     int done = 0;
     double loop_seconds = 0.0;
     s = kf_run(ctx.c, rec.data(), &done, final_state ? state.data() : nullptr, &loop_seconds);
-    if (s.code && s.code != KF_DIVERGED) detail::throw_status(s);
+    if (s.code && s.code != KF_DIVERGED) throw_status(s);
 
     RunHistory h;
     h.points = n;
@@ -125,6 +140,29 @@ inline RunHistory run_fixed_point(const PointCloud& cloud, const LsCoefficients&
             for (int j = 0; j < 4; ++j) (*final_state)[p][j] = state[4 * static_cast<size_t>(p) + j];
     }
     return h;
+}
+
+}  // namespace detail
+
+inline RunHistory run_fixed_point(const PointCloud& cloud, const LsCoefficients& ls,
+                                  const SweepPlan& plan, const SolverConfig& config,
+                                  std::vector<Vec4>* final_state, int device = 0, int n_parts = 1)
+{
+    (void)ls;  // rebuilt on the library side, bit-identically
+    return detail::run_impl(cloud, plan, config, final_state, device, n_parts, 0, nullptr);
+}
+
+/// One process per GPU (e.g. under MPI): every rank calls this with the same
+/// cloud/plan/config and the same NCCL id (rank 0: kf_nccl_unique_id, then
+/// MPI_Bcast of KF_NCCL_ID_BYTES bytes). Every rank gets the full RunHistory;
+/// *final_state receives this rank's owned points (other entries untouched:
+/// gather them with MPI if the whole state is needed).
+inline RunHistory run_fixed_point_rank(const PointCloud& cloud, const SweepPlan& plan,
+                                       const SolverConfig& config, std::vector<Vec4>* final_state,
+                                       int device, int n_ranks, int rank, const unsigned char* nccl_id)
+{
+    if (final_state) final_state->resize(cloud.n());
+    return detail::run_impl(cloud, plan, config, final_state, device, n_ranks, rank, nccl_id);
 }
 
 }  // namespace kinfree::gpu

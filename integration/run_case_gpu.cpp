@@ -4,7 +4,7 @@
 // libkf.so by integration/Makefile. Runs the same case through both and
 // prints one JSON line comparing the two RunHistory records.
 //
-//   run_case_gpu <n_wall> <n_radial> <radius> <variant> <mach> <aoa> <cfl> <iters>
+//   run_case_gpu <n_wall> <n_radial> <radius> <variant> <mach> <aoa> <cfl> <iters> [n_parts]
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -40,7 +40,8 @@ int main(int argc, char** argv)
 
     std::vector<Vec4> s_cpu, s_gpu;
     const RunHistory a = run_fixed_point(cloud, ls, plan, cfg, &s_cpu);
-    const RunHistory b = gpu::run_fixed_point(cloud, ls, plan, cfg, &s_gpu);
+    const int n_parts = argc > 9 ? std::atoi(argv[9]) : 1;
+    const RunHistory b = gpu::run_fixed_point(cloud, ls, plan, cfg, &s_gpu, 0, n_parts);
 
     double max_rel = 0.0, max_cl = 0.0, max_state = 0.0, state_scale = 0.0;
     const size_t m = std::min(a.iters.size(), b.iters.size());

@@ -20,6 +20,9 @@ pytestmark = [pytest.mark.gpu,
     ["48", "12", "12", "anandh", "0.85", "1", "0.2", "40"],
     ["160", "60", "20", "anandh_ad", "0.63", "2", "0.2", "60"],
     ["320", "120", "20", "manish_ad", "0.63", "2", "0.2", "1000"],
+    # domain-decomposed (4 in-process partitions) behind the same adapter
+    ["160", "60", "20", "manish", "0.63", "2", "0.2", "60", "4"],
+    ["320", "120", "20", "manish_ad", "0.63", "2", "0.2", "1000", "3"],
 ])
 def test_reference_run_case_with_gpu_adapter(args):
     out = subprocess.run([BIN] + args, capture_output=True, text=True, timeout=900)
