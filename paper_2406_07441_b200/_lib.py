@@ -30,7 +30,7 @@ EXPORTED = [
     "kf_device_count", "kf_profile_kernels", "kf_measure_fp64_peak",
     "kf_partition_plan", "kf_layout_build", "kf_layout_free", "kf_layout_sizes",
     "kf_layout_arrays", "kf_layout_send", "kf_layout_recv", "kf_create_partitioned",
-    "kf_nccl_unique_id", "kf_create_rank", "kf_n_parts", "kf_owned_points",
+    "kf_nccl_unique_id", "kf_create_rank", "kf_n_parts", "kf_owned_points", "kf_step_host_batch",
 ]
 
 KF_NCCL_ID_BYTES = 128
@@ -102,6 +102,7 @@ def _load():
         "kf_sync_records": (_S, [_vp, _vp, C.c_int, C.POINTER(C.c_int)]),
         "kf_step_host": (_S, [_vp, _vp, _vp, _vp, _vp, _vp]),
         "kf_bench_mode": (_S, [_vp, C.c_int]),
+        "kf_step_host_batch": (_S, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp]),
         "kf_stream": (_vp, [_vp]),
         "kf_launches_per_iteration": (C.c_int, [_vp]),
         "kf_stage_q": (_S, [_vp, _dp, _dp]),

@@ -510,6 +510,19 @@ class Solver:
         _check(st)
         return U_out, _records([rec], 1)[0]
 
+    def step_host_batch(self, U_in, dU_prev_in, U_out, dU_out=None):
+        """len(U_in) independent host-fed steps, pipelined (kf_step_host_batch).
+        Arguments are lists of (n, 4) float64 arrays (pinned for overlap);
+        returns the records."""
+        m = len(U_in)
+        P = C.c_void_p * m
+        pa = lambda xs: P(*[x.ctypes.data if hasattr(x, "ctypes") else x.data_ptr() for x in xs])
+        recs = (L.IterRecord * max(m, 1))()
+        st = lib.kf_step_host_batch(self._h, m, pa(U_in), pa(dU_prev_in), pa(U_out),
+                                    None if dU_out is None else pa(dU_out), recs)
+        _check(st)
+        return _records(recs, m)
+
     def bench_mode(self, on=True):
         _check(lib.kf_bench_mode(self._h, int(bool(on))))
 

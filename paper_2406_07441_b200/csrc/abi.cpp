@@ -483,6 +483,18 @@ kf_status kf_step_host(kf_ctx* ctx, const double* U_in, const double* dU_prev_in
     });
 }
 
+kf_status kf_step_host_batch(kf_ctx* ctx, int m, const double* const* U_in, const double* const* dU_prev_in,
+                             double* const* U_out, double* const* dU_out, kf_iter_record* records)
+{
+    return guarded([&] {
+        std::string reason;
+        int point = -1;
+        const int code = ctx->solver->step_host_batch(m, U_in, dU_prev_in, U_out, dU_out, records, reason, point);
+        if (code != KF_OK) return err(code, reason, point, 1);
+        return ok();
+    });
+}
+
 kf_status kf_bench_mode(kf_ctx* ctx, int mode)
 {
     return guarded([&] {

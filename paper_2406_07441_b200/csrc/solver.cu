@@ -225,6 +225,22 @@ struct Solver::Impl {
     std::vector<cudaEvent_t>* prof_ev = nullptr;
     std::vector<std::string>* prof_names = nullptr;
     ncclComm_t comm = nullptr;
+    // host-fed step pipeline (step_host_batch): double-buffered device
+    // staging in reference order, copy streams and events
+    struct Pipe {
+        bool ready = false;
+        cudaStream_t s_in = nullptr, s_out = nullptr;
+        double4* din[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [buf][U, dU]
+        double4* dout[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+        DevRecord* drec = nullptr;                // [2]
+        unsigned long long* dstat = nullptr;      // [2]
+        DevRecord* hrec = nullptr;                // pinned [cap]
+        unsigned long long* hstat = nullptr;      // pinned [cap]
+        int cap = 0;
+        cudaEvent_t in_ready[2], in_free[2], out_ready[2], out_free[2];
+        cudaGraphExec_t graph = nullptr;
+    } pipe;
+    void ensure_pipe(int m);
 
     Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spec);
     ~Impl();
@@ -372,6 +388,19 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
 
 Solver::Impl::~Impl()
 {
+    if (pipe.ready) {
+        for (int b = 0; b < 2; ++b) {
+            cudaEventDestroy(pipe.in_ready[b]);
+            cudaEventDestroy(pipe.in_free[b]);
+            cudaEventDestroy(pipe.out_ready[b]);
+            cudaEventDestroy(pipe.out_free[b]);
+        }
+        if (pipe.graph) cudaGraphExecDestroy(pipe.graph);
+        if (pipe.hrec) cudaFreeHost(pipe.hrec);
+        if (pipe.hstat) cudaFreeHost(pipe.hstat);
+        cudaStreamDestroy(pipe.s_in);
+        cudaStreamDestroy(pipe.s_out);
+    }
     for (auto& g : graph)
         if (g) cudaGraphExecDestroy(g);
     if (bench_graph) cudaGraphExecDestroy(bench_graph);
@@ -1566,6 +1595,115 @@ int Solver::step_host(const double* U_in, const double* dU_in, double* U_out, do
     int it;
     reason = I.message(key, point, it);
     return KF_DIVERGED;
+}
+
+void Solver::Impl::ensure_pipe(int m)
+{
+    if (!pipe.ready) {
+        ck(cudaStreamCreateWithFlags(&pipe.s_in, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&pipe.s_out, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (int b = 0; b < 2; ++b) {
+            for (int f = 0; f < 2; ++f) {
+                pipe.din[b][f] = dalloc<double4>(std::max(n, 1), owned);
+                pipe.dout[b][f] = dalloc<double4>(std::max(n, 1), owned);
+            }
+            ck(cudaEventCreateWithFlags(&pipe.in_ready[b], cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&pipe.in_free[b], cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&pipe.out_ready[b], cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&pipe.out_free[b], cudaEventDisableTiming), "event");
+            // all buffers start free
+            ck(cudaEventRecord(pipe.in_free[b], s), "event");
+            ck(cudaEventRecord(pipe.out_free[b], pipe.s_out), "event");
+        }
+        pipe.drec = dalloc<DevRecord>(2, owned);
+        pipe.dstat = dalloc<unsigned long long>(2, owned);
+        if (cfg.use_graph) {
+            cudaGraph_t g;
+            ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+            enqueue_iteration(0, 0.0, true);
+            ck(cudaStreamEndCapture(s, &g), "capture end");
+            ck(cudaGraphInstantiate(&pipe.graph, g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+        }
+        pipe.ready = true;
+    }
+    if (m > pipe.cap) {
+        if (pipe.hrec) cudaFreeHost(pipe.hrec);
+        if (pipe.hstat) cudaFreeHost(pipe.hstat);
+        ck(cudaMallocHost(&pipe.hrec, sizeof(DevRecord) * m), "cudaMallocHost");
+        ck(cudaMallocHost(&pipe.hstat, sizeof(unsigned long long) * m), "cudaMallocHost");
+        pipe.cap = m;
+    }
+}
+
+int Solver::step_host_batch(int m, const double* const* U_in, const double* const* dU_in, double* const* U_out,
+                            double* const* dU_out, kf_iter_record* recs, std::string& reason, int& point)
+{
+    Impl& I = *impl_;
+    if (m <= 0) return KF_OK;
+    if (I.transport != kSingle) {  // partitioned contexts: one synchronous step after another
+        for (int k = 0; k < m; ++k) {
+            const int code = step_host(U_in[k], dU_in[k], U_out[k], dU_out ? dU_out[k] : nullptr,
+                                       recs ? recs + k : nullptr, reason, point);
+            if (code != KF_OK) return code;
+        }
+        return KF_OK;
+    }
+    I.ensure_pipe(m);
+    Impl::Pipe& Q = I.pipe;
+    Part& P = I.p0();
+    const size_t bytes = sizeof(double4) * static_cast<size_t>(I.n);
+    for (int k = 0; k < m; ++k) {
+        const int b = k & 1;
+        // inputs of step k -> staging b (free once step k-2 consumed it)
+        ck(cudaStreamWaitEvent(Q.s_in, Q.in_free[b], 0), "wait");
+        if (bytes) {
+            ck(cudaMemcpyAsync(Q.din[b][0], U_in[k], bytes, cudaMemcpyHostToDevice, Q.s_in), "H2D");
+            ck(cudaMemcpyAsync(Q.din[b][1], dU_in[k], bytes, cudaMemcpyHostToDevice, Q.s_in), "H2D");
+        }
+        ck(cudaEventRecord(Q.in_ready[b], Q.s_in), "event");
+        // the iteration
+        ck(cudaStreamWaitEvent(I.s, Q.in_ready[b], 0), "wait");
+        k_to_dev<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(P.D.U[0], Q.din[b][0], P.D.orig, P.n_pad);
+        k_to_dev<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(P.D.dU, Q.din[b][1], P.D.orig, P.n_pad);
+        ck(cudaEventRecord(Q.in_free[b], I.s), "event");
+        k_set_ctrl<<<1, 1, 0, I.s>>>(P.D, 0);
+        if (Q.graph)
+            ck(cudaGraphLaunch(Q.graph, I.s), "graph launch");
+        else
+            I.enqueue_iteration(0, 0.0, true);
+        // outputs of step k -> staging b (free once step k-2's D2H is done)
+        ck(cudaStreamWaitEvent(I.s, Q.out_free[b], 0), "wait");
+        k_to_ref<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(Q.dout[b][0], P.D.U[1], P.D.orig, P.D.kind, P.n_pad);
+        if (dU_out)
+            k_to_ref<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(Q.dout[b][1], P.D.dU, P.D.orig, P.D.kind, P.n_pad);
+        ck(cudaMemcpyAsync(Q.drec + b, P.D.rec, sizeof(DevRecord), cudaMemcpyDeviceToDevice, I.s), "D2D");
+        ck(cudaMemcpyAsync(Q.dstat + b, P.D.status, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, I.s), "D2D");
+        ck(cudaEventRecord(Q.out_ready[b], I.s), "event");
+        ck(cudaStreamWaitEvent(Q.s_out, Q.out_ready[b], 0), "wait");
+        if (bytes) {
+            ck(cudaMemcpyAsync(U_out[k], Q.dout[b][0], bytes, cudaMemcpyDeviceToHost, Q.s_out), "D2H");
+            if (dU_out) ck(cudaMemcpyAsync(dU_out[k], Q.dout[b][1], bytes, cudaMemcpyDeviceToHost, Q.s_out), "D2H");
+        }
+        ck(cudaMemcpyAsync(Q.hrec + k, Q.drec + b, sizeof(DevRecord), cudaMemcpyDeviceToHost, Q.s_out), "D2H");
+        ck(cudaMemcpyAsync(Q.hstat + k, Q.dstat + b, sizeof(unsigned long long), cudaMemcpyDeviceToHost, Q.s_out),
+           "D2H");
+        ck(cudaEventRecord(Q.out_free[b], Q.s_out), "event");
+    }
+    ck(cudaStreamSynchronize(Q.s_out), "step batch sync");
+    ck(cudaStreamSynchronize(I.s), "step batch sync");
+    I.cur = 1;
+    int code = KF_OK;
+    for (int k = 0; k < m; ++k) {
+        if (recs) I.fill_record(recs[k], Q.hrec[k], false);
+        const unsigned long long key = Q.hstat[k];
+        if (code == KF_OK && key != kNoKey && !(key_stage(key) == ST_Q && key_reason(key) == RS_STOP)) {
+            int it;
+            reason = I.message(key, point, it);
+            code = KF_DIVERGED;
+        }
+    }
+    return code;
 }
 
 // ---------------------------------------------------------------- stages
