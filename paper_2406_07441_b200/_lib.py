@@ -31,6 +31,7 @@ EXPORTED = [
     "kf_partition_plan", "kf_layout_build", "kf_layout_free", "kf_layout_sizes",
     "kf_layout_arrays", "kf_layout_send", "kf_layout_recv", "kf_create_partitioned",
     "kf_nccl_unique_id", "kf_create_rank", "kf_n_parts", "kf_owned_points", "kf_step_host_batch",
+    "kf_probe_math",
 ]
 
 KF_NCCL_ID_BYTES = 128
@@ -112,6 +113,7 @@ def _load():
         "kf_stage_update": (_S, [_vp, _dp, _dp, _dp]),
         "kf_stage_forces": (_S, [_vp, _dp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "kf_probe_split_flux": (_S, [C.c_int, _dp, C.c_int, C.c_int, _dp]),
+        "kf_probe_math": (_S, [C.c_int, C.c_int, _dp, _dp, _dp]),
         "kf_probe_jvp_split": (_S, [C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp]),
         "kf_probe_jvp_full": (_S, [C.c_int, _dp, _dp, C.c_int, C.c_int, _dp]),
         "kf_profile_kernels": (_S, [_vp, C.c_int, C.c_char_p, _vp, C.c_int, C.POINTER(C.c_int)]),

@@ -277,6 +277,7 @@ struct Solver::Impl {
                 case 1: k_residual_t<4, false><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
                 case 2: k_residual_t<3, true><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
                 case 3: k_residual_t<4, true><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
+                case 4: k_residual_t<5, true><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
                 default: k_residual_t<3, false><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
             }
             return;
@@ -284,7 +285,8 @@ struct Solver::Impl {
         switch (flux_variant) {
             case 1: k_residual<4, false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
             case 2: k_residual<3, true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
-            case 3: k_residual<4, true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
+            case 3:
+            case 4: k_residual<4, true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
             default: k_residual<3, false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
         }
     }
@@ -340,7 +342,7 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // A/B switch for the residual kernel (register cap x arithmetic)
         const char* env = std::getenv("KF_FLUX_KERNEL");
         const std::string v = env ? env : "m4fast";
-        flux_variant = v == "m3" ? 0 : v == "m4" ? 1 : v == "m3fast" ? 2 : 3;
+        flux_variant = v == "m3" ? 0 : v == "m4" ? 1 : v == "m3fast" ? 2 : v == "m5fast" ? 4 : 3;
         // A/B switch for the neighbour gathers of the gradient/residual kernels
         const char* g = std::getenv("KF_GATHER");
         gather = (g && std::string(g) == "ell") ? 0 : 1;
@@ -558,6 +560,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     std::vector<double2> lsfd(n_pad, make_double2(1, 1)), xy(n_pad, make_double2(0, 0));
     auto form = [](double A, double B, double Dn, double u, double v) { return (A * u - B * v) / Dn; };
     std::vector<unsigned char> emask(c.nbr.idx.size(), 0);  // split mask per nbr entry
+    std::vector<double4> ew(c.nbr.idx.size(), make_double4(0, 0, 0, 0));  // split weights per entry (device order)
     std::vector<int> wall_slot_of(c.n, -1);
     for (int k = 0; k < W && W >= 3; ++k) wall_slot_of[c.wall_ids[k]] = k;
     P.nnz_w = 0;
@@ -631,6 +634,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             const size_t e = static_cast<size_t>(slice_off[pn >> 5]) + 32 * kk + (pn & 31);
             e_id[e] = static_cast<unsigned>(inv[i]) | (mask << 28);
             emask[k] = static_cast<unsigned char>(mask);
+            ew[k] = make_double4(w[slot_of[0]], w[slot_of[1]], w[slot_of[2]], w[slot_of[3]]);
             P.nnz_w += __builtin_popcount(mask);
         }
         hmin[pn] = h;
@@ -667,6 +671,8 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     // staged set (own points + their stencil neighbours) stays <= kHaloCap
     std::vector<int> tpts, thoff(1, 0), thalo, teoff(1, 0);
     std::vector<unsigned short> tell;
+    std::vector<double> tw;                  // streamed split weights (residual)
+    std::vector<long long> twoff(1, 0);
     std::vector<double4> tlsf, tlsA, tlsB, tlsD;
     std::vector<double2> tlsfd;
     int nh_max = 1;
@@ -734,6 +740,27 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             }
             tell.insert(tell.end(), ent.begin(), ent.end());
             teoff.push_back(static_cast<int>(tell.size()));
+            // the nonzero split weights of each lane in consumption order
+            // (column, then direction), column-major over the tile
+            {
+                std::vector<std::vector<double>> lw(pts.size());
+                size_t ww = 0;
+                for (size_t t = 0; t < pts.size(); ++t) {
+                    const int o = P.perm[pts[t]];
+                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
+                        const double4 w4 = ew[k];
+                        const double wd[4] = {w4.x, w4.y, w4.z, w4.w};
+                        for (int d = 0; d < 4; ++d)
+                            if (emask[k] >> d & 1u) lw[t].push_back(wd[d]);
+                    }
+                    ww = std::max(ww, lw[t].size());
+                }
+                const size_t base = tw.size();
+                tw.resize(base + ww * kThreads, 0.0);
+                for (size_t t = 0; t < pts.size(); ++t)
+                    for (size_t j = 0; j < lw[t].size(); ++j) tw[base + j * kThreads + t] = lw[t][j];
+                twoff.push_back(static_cast<long long>(tw.size()));
+            }
             thoff.push_back(static_cast<int>(thalo.size()));
             nh_max = std::max(nh_max, ns);
             for (int t = 0; t < kThreads; ++t) {
@@ -759,6 +786,8 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             teoff.push_back(0);
             thalo.push_back(0);
             tell.push_back(0);
+            twoff.push_back(0);
+            tw.push_back(0.0);
             tcount = 1;
         }
         P.n_tiles = tcount;
@@ -868,6 +897,12 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         D.t_lsA = up4(tlsA);
         D.t_lsB = up4(tlsB);
         D.t_lsD = up4(tlsD);
+        double* d_tw = dalloc<double>(tw.size(), owned);
+        up(d_tw, tw);
+        D.t_w = d_tw;
+        long long* d_twoff = dalloc<long long>(twoff.size(), owned);
+        up(d_twoff, twoff);
+        D.t_woff = d_twoff;
         const size_t ent_bytes = static_cast<size_t>(P.w_max) * kThreads * sizeof(unsigned short);
         P.tile_smem = static_cast<size_t>(kTileUnits) * P.nh_cap * sizeof(double2) + ent_bytes;
         P.tile_smem1 = static_cast<size_t>(3) * P.nh_cap * sizeof(double2) + ent_bytes;
@@ -881,6 +916,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         ck(cudaFuncSetAttribute(k_residual_t<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t<5, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
     }
 
     for (int b = 0; b < 2; ++b) {
@@ -1910,6 +1946,26 @@ void probe(int mode, int n, const double* U, const double* dU, int axis, int sig
     cudaFree(dst);
 }
 }  // namespace
+
+void probe_math(int n, int which, const double* x, double* lib, double* mine)
+{
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw SolverError(KF_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    double *dx = nullptr, *dl = nullptr, *dm = nullptr;
+    const size_t b = sizeof(double) * std::max(n, 1);
+    ck(cudaMalloc(&dx, b), "cudaMalloc");
+    ck(cudaMalloc(&dl, b), "cudaMalloc");
+    ck(cudaMalloc(&dm, b), "cudaMalloc");
+    ck(cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+    k_mathprobe<<<blocks_for(n, 256), 256>>>(n, which, dx, dl, dm);
+    ck(cudaGetLastError(), "mathprobe launch");
+    ck(cudaMemcpy(lib, dl, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(mine, dm, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(dx);
+    cudaFree(dl);
+    cudaFree(dm);
+}
 
 void probe_split_flux(int n, const double* U, int axis, int sign, double* G)
 {
