@@ -648,6 +648,47 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         }
         if (c.kind[o] == kWall) wslot[pn] = wall_slot_of[o];
     }
+    // sweep weight streams: for every owned point, the split weights the
+    // forward sweep consumes (neighbours of a lower colour, nonzero weight)
+    // and those the backward sweep consumes (higher colour), each in
+    // gather_products' consumption order (column, then direction); sliced
+    // ELL per 32-point slice (column j of lane l at off[slice] + 32 j + l)
+    std::vector<double> swv[2];
+    std::vector<int> swoff[2];
+    {
+        std::vector<int> colour_of(n_pad, 0);
+        for (int g = 0; g < C; ++g)
+            for (int pn = P.gs[g]; pn < P.ge[g]; ++pn) colour_of[pn] = g;
+        for (int dir = 0; dir < 2; ++dir) {
+            swoff[dir].assign(n_slices + 1, 0);
+            std::vector<std::vector<double>> lane(32);
+            for (int sl = 0; sl < n_slices; ++sl) {
+                size_t w = 0;
+                for (int l = 0; l < 32; ++l) {
+                    lane[l].clear();
+                    const int pn = sl * 32 + l;
+                    const int o = P.perm[pn];
+                    if (o < 0 || P.ghost[pn]) continue;
+                    const int g = colour_of[pn];
+                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
+                        const int i = inv[c.nbr.idx[k]];
+                        const bool use = dir == 0 ? i < P.gs[g] : i >= P.ge[g];
+                        if (!use || !emask[k]) continue;
+                        const double4 w4 = ew[k];
+                        const double wd[4] = {w4.x, w4.y, w4.z, w4.w};
+                        for (int d = 0; d < 4; ++d)
+                            if (emask[k] >> d & 1u) lane[l].push_back(wd[d]);
+                    }
+                    w = std::max(w, lane[l].size());
+                }
+                const size_t base = swv[dir].size();
+                swv[dir].resize(base + 32 * w, 0.0);
+                for (int l = 0; l < 32; ++l)
+                    for (size_t j = 0; j < lane[l].size(); ++j) swv[dir][base + 32 * j + l] = lane[l][j];
+                swoff[dir][sl + 1] = static_cast<int>(swv[dir].size());
+            }
+        }
+    }
     // processing order of the point-parallel kernels: owned slices sorted by
     // the Morton code of their first point, so the resident front of a launch
     // is spatially compact across all colours (L2 reuse of the gathers)
@@ -856,6 +897,14 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     unsigned* d_eid = dalloc<unsigned>(n_e, owned);
     up(d_eid, e_id);
     D.e_id = d_eid;
+    for (int dir = 0; dir < 2; ++dir) {
+        double* d_w = dalloc<double>(swv[dir].size(), owned);
+        up(d_w, swv[dir]);
+        D.sw[dir] = d_w;
+        int* d_o = dalloc<int>(swoff[dir].size(), owned);
+        up(d_o, swoff[dir]);
+        D.sw_off[dir] = d_o;
+    }
     auto up4 = [&](const std::vector<double4>& h) {
         double4* d = dalloc<double4>(h.size(), owned);
         up(d, h);
