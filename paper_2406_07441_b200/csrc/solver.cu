@@ -751,30 +751,81 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                 pts.push_back(pn);
                 ++next;
             }
-            if (hcount > 4095) throw SolverError(KF_CONFIG, "stencil too large for a 12-bit tile slot");
-            // slots: own points first (lane order), then neighbours by first use
-            int ns = 0;
-            auto slot_of = [&](int id) {
-                if (sstamp[id] != tcount) {
-                    sstamp[id] = tcount;
-                    slot[id] = ns++;
-                    thalo.push_back(id);
-                }
-                return slot[id];
-            };
-            for (int pn : pts) slot_of(pn);
+            if (hcount + 8 * 64 > 4095) throw SolverError(KF_CONFIG, "stencil too large for a 12-bit tile slot");
+            // slots: own points first (slot = lane); every halo record gets a
+            // bank class (slot mod 8), chosen greedily so that the 8 lanes of
+            // a quarter-warp reading one stencil column touch distinct 16-B
+            // bank groups (the LDS.128 reads of k_grad_t / k_residual_t);
+            // unused slots of the class grid stage a dummy record
+            const int m = static_cast<int>(pts.size());
             int W = 0;
             for (int pn : pts) W = std::max(W, c.nbr.degree(P.perm[pn]));
             P.w_max = std::max(P.w_max, W);
+            for (int t = 0; t < m; ++t) {
+                sstamp[pts[t]] = tcount;
+                slot[pts[t]] = t;
+            }
+            std::vector<int> hid;                     // halo records, first-use order
+            std::vector<std::vector<int>> hgroups;    // their (column, quarter-warp) groups
+            std::vector<unsigned char> gmask(static_cast<size_t>(W) * (kThreads / 8), 0);
+            for (int t = 0; t < m; ++t) {
+                const int o = P.perm[pts[t]];
+                for (int kk = 0; kk < c.nbr.degree(o); ++kk) {
+                    const int id = inv[c.nbr.idx[c.nbr.off[o] + kk]];
+                    const int g = kk * (kThreads / 8) + (t >> 3);
+                    if (sstamp[id] == tcount && slot[id] >= 0 && slot[id] < m) {  // own point
+                        gmask[g] |= static_cast<unsigned char>(1u << (slot[id] & 7));
+                        continue;
+                    }
+                    if (sstamp[id] != tcount) {
+                        sstamp[id] = tcount;
+                        slot[id] = -1 - static_cast<int>(hid.size());  // halo index, encoded
+                        hid.push_back(id);
+                        hgroups.emplace_back();
+                    }
+                    std::vector<int>& hg = hgroups[-1 - slot[id]];
+                    if (hg.empty() || hg.back() != g) hg.push_back(g);
+                }
+            }
+            const int base = (m + 7) & ~7;
+            int cls_count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            std::vector<int> hslot(hid.size());
+            int ns = m;
+            for (size_t h = 0; h < hid.size(); ++h) {
+                int best = 0, best_cost = 1 << 30;
+                for (int b = 0; b < 8; ++b) {
+                    int cost = 0;
+                    for (int g : hgroups[h]) cost += (gmask[g] >> b) & 1;
+                    cost = cost * 4096 + cls_count[b];
+                    if (cost < best_cost) {
+                        best_cost = cost;
+                        best = b;
+                    }
+                }
+                for (int g : hgroups[h]) gmask[g] |= static_cast<unsigned char>(1u << best);
+                hslot[h] = base + 8 * cls_count[best] + best;
+                ++cls_count[best];
+                ns = std::max(ns, hslot[h] + 1);
+            }
+            if (ns > 4096) throw SolverError(KF_CONFIG, "tile slots exceed the 12-bit entry field");
+            {
+                const size_t t0 = thalo.size();
+                thalo.resize(t0 + ns, P.perm[pts[0]] >= 0 ? pts[0] : 0);
+                for (int t = 0; t < m; ++t) thalo[t0 + t] = pts[t];
+                for (size_t h = 0; h < hid.size(); ++h) {
+                    thalo[t0 + hslot[h]] = hid[h];
+                    slot[hid[h]] = hslot[h];
+                }
+            }
             std::vector<unsigned short> ent(static_cast<size_t>(W) * kThreads, 0);
-            for (int t = 0; t < static_cast<int>(pts.size()); ++t) {
+            for (int t = 0; t < m; ++t) {
                 const int o = P.perm[pts[t]];
                 const int deg = c.nbr.degree(o);
                 for (int kk = 0; kk < W; ++kk) {
                     unsigned e = static_cast<unsigned>(t);  // padding: self, no split
                     if (kk < deg) {
                         const int k = c.nbr.off[o] + kk;
-                        e = static_cast<unsigned>(slot_of(inv[c.nbr.idx[k]])) | (unsigned(emask[k]) << 12);
+                        e = static_cast<unsigned>(slot[inv[c.nbr.idx[k]]]) | (unsigned(emask[k]) << 12);
                     }
                     ent[static_cast<size_t>(kk) * kThreads + t] = static_cast<unsigned short>(e);
                 }
