@@ -148,7 +148,7 @@ enum Transport : int { kSingle = 0, kInProc = 1, kNccl = 2 };
 
 // staged records per tile (own points + stencil neighbours); 767 x 14 doubles
 // = 86 KB of shared memory at most (NACA O-grids need <= 372)
-constexpr int kHaloCap = 767;
+constexpr int kHaloCap = 6 * kTile - 1;
 constexpr size_t kMaxTileSmem = 200 * 1024;
 
 }  // namespace
@@ -259,9 +259,9 @@ struct Solver::Impl {
     {
         if (gather) {
             if (first)
-                k_grad_t<true><<<P.n_tiles, kThreads, P.tile_smem1, s>>>(P.D, src, dst);
+                k_grad_t<true><<<P.n_tiles, kTile, P.tile_smem1, s>>>(P.D, src, dst);
             else
-                k_grad_t<false><<<P.n_tiles, kThreads, P.tile_smem, s>>>(P.D, src, dst);
+                k_grad_t<false><<<P.n_tiles, kTile, P.tile_smem, s>>>(P.D, src, dst);
             return;
         }
         if (first)
@@ -274,11 +274,11 @@ struct Solver::Impl {
         if (gather) {
             const size_t sm = P.tile_smem;
             switch (flux_variant) {
-                case 1: k_residual_t<4, false><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
-                case 2: k_residual_t<3, true><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
-                case 3: k_residual_t<4, true><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
-                case 4: k_residual_t<5, true><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
-                default: k_residual_t<3, false><<<P.n_tiles, kThreads, sm, s>>>(P.D, gslot, 0); break;
+                case 1: k_residual_t<4, false><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
+                case 2: k_residual_t<3, true><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
+                case 3: k_residual_t<4, true><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
+                case 4: k_residual_t<5, true><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
+                default: k_residual_t<3, false><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
             }
             return;
         }
@@ -708,7 +708,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     }
 
     // ---- SMEM-staged tiles of the gradient / residual kernels: owned points
-    // in Morton order, greedily cut into tiles of <= kThreads points whose
+    // in Morton order, greedily cut into tiles of <= kTile points whose
     // staged set (own points + their stencil neighbours) stays <= kHaloCap
     std::vector<int> tpts, thoff(1, 0), thalo, teoff(1, 0);
     std::vector<unsigned short> tell;
@@ -731,7 +731,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         while (next < own.size()) {
             pts.clear();
             int hcount = 0;
-            while (next < own.size() && static_cast<int>(pts.size()) < kThreads) {
+            while (next < own.size() && static_cast<int>(pts.size()) < kTile) {
                 const int pn = own[next];
                 const int o = P.perm[pn];
                 added.clear();
@@ -767,12 +767,12 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             }
             std::vector<int> hid;                     // halo records, first-use order
             std::vector<std::vector<int>> hgroups;    // their (column, quarter-warp) groups
-            std::vector<unsigned char> gmask(static_cast<size_t>(W) * (kThreads / 8), 0);
+            std::vector<unsigned char> gmask(static_cast<size_t>(W) * (kTile / 8), 0);
             for (int t = 0; t < m; ++t) {
                 const int o = P.perm[pts[t]];
                 for (int kk = 0; kk < c.nbr.degree(o); ++kk) {
                     const int id = inv[c.nbr.idx[c.nbr.off[o] + kk]];
-                    const int g = kk * (kThreads / 8) + (t >> 3);
+                    const int g = kk * (kTile / 8) + (t >> 3);
                     if (sstamp[id] == tcount && slot[id] >= 0 && slot[id] < m) {  // own point
                         gmask[g] |= static_cast<unsigned char>(1u << (slot[id] & 7));
                         continue;
@@ -817,7 +817,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                     slot[hid[h]] = hslot[h];
                 }
             }
-            std::vector<unsigned short> ent(static_cast<size_t>(W) * kThreads, 0);
+            std::vector<unsigned short> ent(static_cast<size_t>(W) * kTile, 0);
             for (int t = 0; t < m; ++t) {
                 const int o = P.perm[pts[t]];
                 const int deg = c.nbr.degree(o);
@@ -827,7 +827,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                         const int k = c.nbr.off[o] + kk;
                         e = static_cast<unsigned>(slot[inv[c.nbr.idx[k]]]) | (unsigned(emask[k]) << 12);
                     }
-                    ent[static_cast<size_t>(kk) * kThreads + t] = static_cast<unsigned short>(e);
+                    ent[static_cast<size_t>(kk) * kTile + t] = static_cast<unsigned short>(e);
                 }
             }
             tell.insert(tell.end(), ent.begin(), ent.end());
@@ -848,14 +848,14 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                     ww = std::max(ww, lw[t].size());
                 }
                 const size_t base = tw.size();
-                tw.resize(base + ww * kThreads, 0.0);
+                tw.resize(base + ww * kTile, 0.0);
                 for (size_t t = 0; t < pts.size(); ++t)
-                    for (size_t j = 0; j < lw[t].size(); ++j) tw[base + j * kThreads + t] = lw[t][j];
+                    for (size_t j = 0; j < lw[t].size(); ++j) tw[base + j * kTile + t] = lw[t][j];
                 twoff.push_back(static_cast<long long>(tw.size()));
             }
             thoff.push_back(static_cast<int>(thalo.size()));
             nh_max = std::max(nh_max, ns);
-            for (int t = 0; t < kThreads; ++t) {
+            for (int t = 0; t < kTile; ++t) {
                 const bool real = t < static_cast<int>(pts.size());
                 const int pn = real ? pts[t] : 0;
                 tpts.push_back(real ? pn : -1);
@@ -868,12 +868,12 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             ++tcount;
         }
         if (tcount == 0) {  // empty partition: one idle tile
-            tpts.assign(kThreads, -1);
-            tlsf.assign(kThreads, make_double4(0, 0, 0, 0));
-            tlsfd.assign(kThreads, make_double2(1, 1));
-            tlsA.assign(kThreads, make_double4(0, 0, 0, 0));
+            tpts.assign(kTile, -1);
+            tlsf.assign(kTile, make_double4(0, 0, 0, 0));
+            tlsfd.assign(kTile, make_double2(1, 1));
+            tlsA.assign(kTile, make_double4(0, 0, 0, 0));
             tlsB = tlsA;
-            tlsD.assign(kThreads, make_double4(1, 1, 1, 1));
+            tlsD.assign(kTile, make_double4(1, 1, 1, 1));
             thoff.push_back(0);
             teoff.push_back(0);
             thalo.push_back(0);
@@ -1003,7 +1003,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         long long* d_twoff = dalloc<long long>(twoff.size(), owned);
         up(d_twoff, twoff);
         D.t_woff = d_twoff;
-        const size_t ent_bytes = static_cast<size_t>(P.w_max) * kThreads * sizeof(unsigned short);
+        const size_t ent_bytes = static_cast<size_t>(P.w_max) * kTile * sizeof(unsigned short);
         P.tile_smem = static_cast<size_t>(kTileUnits) * P.nh_cap * sizeof(double2) + ent_bytes;
         P.tile_smem1 = static_cast<size_t>(3) * P.nh_cap * sizeof(double2) + ent_bytes;
         if (P.tile_smem > kMaxTileSmem) throw SolverError(KF_CONFIG, "tile staging exceeds shared memory");
