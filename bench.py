@@ -48,6 +48,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# BASELINE.json configs (SURVEY.md §8(d) clouds); 2 is the bench workload,
+# the others are reachable with --case for evidence runs
+CASES = {
+    2: dict(digits="0012", n_wall=1280, n_radial=500, radius=20.0, mach=0.85, aoa=1.0, cfl=0.2,
+            variant="manish_ad"),
+    3: dict(digits="0012", n_wall=2560, n_radial=960, radius=20.0, mach=1.2, aoa=0.0, cfl=0.2,
+            variant="anandh_ad"),
+    4: dict(digits="0012", n_wall=5120, n_radial=1920, radius=20.0, mach=0.63, aoa=2.0, cfl=0.2,
+            variant="manish_ad"),
+    5: dict(digits="0012", n_wall=10240, n_radial=3920, radius=20.0, mach=0.63, aoa=2.0, cfl=0.2,
+            variant="manish_ad"),
+}
 CASE = dict(digits="0012", n_wall=1280, n_radial=500, radius=20.0, mach=0.85, aoa=1.0, cfl=0.2,
             variant="manish_ad")
 METRIC = "Mpoint-iter/s (FP64 LU-SGS+AD) and time-to-residual-drop, NACA 0012 clouds"
@@ -214,11 +226,11 @@ def time_to_drop(kf, decades=1.0, with_cpu=True):
     return out
 
 
-def case_for(world, points=None):
+def case_for(world, points=None, case=2):
     """The bench workload at `world` GPUs: config 2 at N=1; the cloud grows
     with N in the wall direction (weak scaling, ~640,000 points per GPU)."""
-    spec = dict(CASE)
-    spec["n_wall"] = CASE["n_wall"] * max(world, 1)
+    spec = dict(CASES[case])
+    spec["n_wall"] = spec["n_wall"] * max(world, 1)
     if points:
         nw, nr = points.split(":")
         spec["n_wall"], spec["n_radial"] = int(nw), int(nr)
@@ -230,7 +242,7 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = cpu_cores()
-    spec = case_for(world, args.points)
+    spec = case_for(world, args.points, args.case)
     secs, n, kind = reference_cpu(args.warmup + args.steps, threads, spec)
     timed = secs[args.warmup:args.warmup + args.steps] or secs
     total = float(np.sum(timed))
@@ -240,8 +252,8 @@ def run_reference_arm(args):
         "steps": len(timed), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(timed),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated NACA 0012 O-grid, deterministic)",
-        "config": {"workload": f"naca0012:{spec['n_wall']}:{spec['n_radial']}:20 M0.85 AoA1 manish_ad CFL0.2, "
-                               "one fixed-point iteration",
+        "config": {"workload": f"naca0012:{spec['n_wall']}:{spec['n_radial']}:20 M{spec['mach']} "
+                               f"AoA{spec['aoa']:g} {spec['variant']} CFL{spec['cfl']}, one fixed-point iteration",
                    "points": n, "parallelism": "cpu-openmp"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{len(timed)} reference iterations of the same case (runs restarted "
@@ -263,6 +275,8 @@ def main():
                     help="run a few steps for ncu (no JSON line)")
     ap.add_argument("--points", default=None, help="override cloud n_wall:n_radial")
     ap.add_argument("--parts", type=int, default=1, help="in-process partitions on one GPU")
+    ap.add_argument("--case", type=int, default=2, choices=sorted(CASES),
+                    help="BASELINE.json config whose cloud/case to time (default 2, the bench workload)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -277,7 +291,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    spec = case_for(world, args.points)
+    spec = case_for(world, args.points, args.case)
 
     cloud = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
     N = cloud.n()
@@ -293,6 +307,9 @@ def main():
     solver.iterate_async(WARM_ITERS)
     recs, st = solver.sync_records()
     assert st.code == 0 and len(recs) == WARM_ITERS, st.reason
+    # the resident iteration-5 state: every timed step (device and e2e) runs
+    # iteration 6 from it
+    U0, dU0 = solver.get_state(with_dU=True)
     solver.bench_mode(True)
     stream = torch.cuda.ExternalStream(solver.stream_ptr, device=torch.device("cuda", local))
 
@@ -329,8 +346,6 @@ def main():
     launches = solver.launches_per_iteration * args.steps
 
     # ---- end to end through the C ABI with pinned host buffers
-    U0, dU0 = solver.get_state(with_dU=True)
-    solver.bench_mode(True)
     Uh = torch.from_numpy(U0).pin_memory()
     dUh = torch.from_numpy(dU0).pin_memory()
     Uo = torch.empty_like(Uh).pin_memory()
@@ -450,8 +465,10 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
         "config": {
-            "workload": f"naca0012:{spec['n_wall']}:{spec['n_radial']}:20 M0.85 AoA1 manish_ad CFL0.2 n_inner3, "
-                        "one fixed-point iteration (re-run of iteration 6 from the resident iteration-5 state)",
+            "workload": f"naca0012:{spec['n_wall']}:{spec['n_radial']}:20 M{spec['mach']} AoA{spec['aoa']:g} "
+                        f"{spec['variant']} CFL{spec['cfl']} n_inner3, one fixed-point iteration (re-run of "
+                        "iteration 6 from the resident iteration-5 state)",
+            "baseline_config": args.case,
             "points": N, "colours": int(kf.color_points(cloud).n_colors),
             "parallelism": (f"domain-decomposition x{world} (angular wedges, NCCL halos)" if world > 1 else
                             f"single-gpu, {args.parts} in-process partitions" if args.parts > 1 else "single-gpu"),
@@ -487,7 +504,7 @@ def main():
             "value": n_ref / float(np.median(secs)) / 1e6, "unit": UNIT, "cores": cpu_cores(),
             "kind": kind, "sample": f"{len(secs)} iterations of the same case on the host "
                                     "(median per-iteration time, warm-up iteration excluded)"}
-    if rank == 0 and world == 1 and args.parts == 1:
+    if rank == 0 and world == 1 and args.parts == 1 and args.case == 2:
         line["time_to_drop"] = time_to_drop(kf, 1.0, with_cpu=not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line), flush=True)
