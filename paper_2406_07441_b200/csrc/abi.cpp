@@ -325,14 +325,14 @@ kf_status kf_create_rank(const kf_cloud* cloud, const kf_config* cfg, int n_rank
     kfb::PartitionSpec spec;
     spec.n_parts = n_ranks;
     spec.mode = mode;
-    spec.nccl = n_ranks > 1;
+    spec.nccl = 1;  // also for n_ranks == 1: the NCCL transport with one rank
     spec.rank = rank;
     spec.nccl_id = nccl_id;
-    if (n_ranks > 1 && !nccl_id) {
+    if (!nccl_id) {
         *out = nullptr;
         return err(KF_CONFIG, "kf_create_rank: missing NCCL unique id");
     }
-    if (n_ranks == 1 && rank != 0) {
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) {
         *out = nullptr;
         return err(KF_CONFIG, "rank out of range");
     }

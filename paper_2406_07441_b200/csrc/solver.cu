@@ -244,7 +244,7 @@ struct Solver::Impl {
 
     Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spec);
     ~Impl();
-    bool multi() const { return n_rows > 1; }
+    bool multi() const { return transport != kSingle; }
     Part& p0() { return parts[0]; }
     void pack(const Cloud& c, const LocalLayout& L, const std::vector<uint64_t>& code,
               const std::vector<double>& oty, const std::vector<double>& otx, double* red_shared,
@@ -315,7 +315,7 @@ struct Solver::Impl {
     void fill_record(kf_iter_record& out, const DevRecord& r, bool accumulate);
     void require_single(const char* what) const
     {
-        if (n_rows != 1)
+        if (transport != kSingle)
             throw SolverError(KF_CONFIG, std::string(what) + ": stage hooks need an unpartitioned context");
     }
 };
@@ -335,7 +335,7 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
     C = std::max(c.n_colors, 1);
     if (spec.n_parts < 1) throw SolverError(KF_CONFIG, "n_parts must be >= 1");
     n_rows = spec.n_parts;
-    transport = spec.n_parts == 1 ? kSingle : (spec.nccl ? kNccl : kInProc);
+    transport = spec.nccl ? kNccl : (spec.n_parts == 1 ? kSingle : kInProc);
     if (transport == kNccl && (spec.rank < 0 || spec.rank >= spec.n_parts))
         throw SolverError(KF_CONFIG, "rank out of range");
     {
@@ -1088,7 +1088,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     D.forces_err = forces_err;
     D.n_rows = n_rows;
     const size_t red_len = static_cast<size_t>(W) + kRowStride * static_cast<size_t>(n_rows);
-    if (n_rows == 1) {
+    if (transport == kSingle) {
         D.cp = dalloc<double>(std::max(W, 1), owned);
         D.red = nullptr;
     } else if (red_shared) {

@@ -73,3 +73,15 @@ def test_singular_interior_stencil_refused():
                                               [[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]]))
     with pytest.raises(kf.KinfreeError, match="singular least-squares stencil"):
         kf.Solver(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD))
+
+
+def test_create_rank_validates_arguments():
+    import ctypes as C
+    from paper_2406_07441_b200 import _lib
+    c = kf.generate_naca_ogrid("0012", 32, 8, 10.0)
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.ManishAD).to_c()
+    h = C.c_void_p()
+    st = _lib.lib.kf_create_rank(c.handle, C.byref(cfg), 2, 0, 0, None, C.byref(h))
+    assert st.code == _lib.KF_CONFIG and b"NCCL unique id" in st.reason
+    st = _lib.lib.kf_create_rank(c.handle, C.byref(cfg), 2, 2, 0, b"x" * 128, C.byref(h))
+    assert st.code == _lib.KF_CONFIG and b"rank out of range" in st.reason

@@ -114,3 +114,26 @@ def test_partitioned_contexts_refuse_stage_hooks(small):
     s = kf.Solver(small, cfg("manish_ad"), n_parts=2)
     with pytest.raises(kf.ConfigError):
         s.q(np.ones((small.n(), 4)))
+
+
+def test_nccl_transport_single_rank(small):
+    """The NCCL transport with one rank (the path every rank of a multi-GPU
+    run takes: NCCL bound at run time, communicator, halo groups and the
+    per-iteration ncclAllReduce captured in the iteration graph, reduced
+    records through k_finalize<MULTI>) against the unpartitioned solver."""
+    one = kf.Solver(small, cfg("manish_ad", n_iterations=40)).run()
+    s = kf.Solver.for_rank(small, cfg("manish_ad", n_iterations=40), 1, 0, kf.nccl_unique_id())
+    assert s.n_parts == 1 and s.owned_points == small.n()
+    r = s.run()
+    assert len(r.iters) == len(one.iters) and r.abort_reason == one.abort_reason
+    assert relmax(r.residual, one.residual) <= 1e-13
+    assert np.array_equal(r.cl, one.cl)
+    assert np.array_equal(r.final_state, one.final_state)
+    # stepping and the host-fed step through the same transport
+    s.reset()
+    s.iterate_async(3)
+    U, dU = s.get_state(with_dU=True)
+    got, rec = s.step_host(U, dU)
+    ref = kf.Solver(small, cfg("manish_ad", n_iterations=40))
+    want, rec1 = ref.step_host(U, dU)
+    assert np.array_equal(got, want)
