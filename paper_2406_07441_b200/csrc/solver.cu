@@ -725,14 +725,36 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             if (P.perm[pn] >= 0 && !P.ghost[pn]) own.push_back(pn);
         std::stable_sort(own.begin(), own.end(), [&](int a, int b) { return code[P.perm[a]] < code[P.perm[b]]; });
         std::vector<int> stamp(n_pad, -1), sstamp(n_pad, -1), slot(n_pad, -1);
-        size_t next = 0;
+        // tile growth: breadth-first over the stencil graph from the first
+        // free point in Morton order (compact tiles: staged/own ~1.5 on an
+        // O-grid instead of ~1.9 for Morton chunks), topped up from the next
+        // free seeds when a region runs out; KF_TILE_ORDER=morton = chunks
+        const char* to = std::getenv("KF_TILE_ORDER");
+        const bool bfs = !(to && std::string(to) == "morton");
+        std::vector<char> taken(n_pad, 0);
+        std::vector<int> qstamp(n_pad, -1), fifo;
+        size_t seed = 0;
         int tcount = 0;
         std::vector<int> pts, added;
-        while (next < own.size()) {
+        auto next_seed = [&]() {
+            while (seed < own.size() && taken[own[seed]]) ++seed;
+            return seed < own.size() ? own[seed] : -1;
+        };
+        while (next_seed() >= 0) {
             pts.clear();
             int hcount = 0;
-            while (next < own.size() && static_cast<int>(pts.size()) < kTile) {
-                const int pn = own[next];
+            fifo.clear();
+            size_t head = 0;
+            bool full = false;
+            while (!full && static_cast<int>(pts.size()) < kTile) {
+                if (head == fifo.size()) {  // region exhausted (or start): next seed
+                    const int sd = next_seed();
+                    if (sd < 0) break;
+                    qstamp[sd] = tcount;
+                    fifo.push_back(sd);
+                }
+                const int pn = fifo[head++];
+                if (taken[pn]) continue;
                 const int o = P.perm[pn];
                 added.clear();
                 auto touch = [&](int id) {
@@ -745,11 +767,23 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                 for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) touch(inv[c.nbr.idx[k]]);
                 if (hcount + static_cast<int>(added.size()) > halo_cap && !pts.empty()) {
                     for (int id : added) stamp[id] = -1;
+                    full = true;
                     break;
                 }
                 hcount += static_cast<int>(added.size());
                 pts.push_back(pn);
-                ++next;
+                taken[pn] = 1;
+                if (!bfs) {
+                    ++seed;  // Morton chunks: the next point in order
+                    continue;
+                }
+                for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
+                    const int li = inv[c.nbr.idx[k]];
+                    if (li >= 0 && !P.ghost[li] && !taken[li] && qstamp[li] != tcount) {
+                        qstamp[li] = tcount;
+                        fifo.push_back(li);
+                    }
+                }
             }
             if (hcount + 8 * 64 > 4095) throw SolverError(KF_CONFIG, "stencil too large for a 12-bit tile slot");
             // slots: own points first (slot = lane); every halo record gets a
