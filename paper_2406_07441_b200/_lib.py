@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkf.so")
+# KF_LIB_PATH: an alternative in-tree build (A/B experiments of build flags)
+LIB_PATH = os.environ.get("KF_LIB_PATH") or os.path.join(HERE, "libkf.so")
 
 KF_OK, KF_INVALID_STATE, KF_INVALID_INCREMENT, KF_DIVERGED, KF_CONFIG, KF_CUDA, KF_RUNTIME = range(7)
 
