@@ -4,6 +4,10 @@
 // reference's; only the storage (flat CSR) differs.
 #include "cloud.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cctype>
 #include <cerrno>
@@ -179,34 +183,56 @@ bool report_singular(const Cloud& c, int p, const int* st, int m)
 
 void split_stencils(Cloud& c)
 {
-    for (auto& s : c.split) {
-        s.off.assign(c.n + 1, 0);
-        s.idx.clear();
-        s.idx.reserve(c.nbr.idx.size() * 5 / 8 + 8);
-    }
-    c.empty_points.clear();
-    c.singular_points.clear();
-    for (int p = 0; p < c.n; ++p) {
-        for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1]; ++k) {
-            const int q = c.nbr.idx[k];
-            const double dx = c.x[q] - c.x[p];
-            const double dy = c.y[q] - c.y[p];
-            if (dx >= 0.0) c.split[kXpos].idx.push_back(q);
-            if (dx <= 0.0) c.split[kXneg].idx.push_back(q);
-            if (dy >= 0.0) c.split[kYpos].idx.push_back(q);
-            if (dy <= 0.0) c.split[kYneg].idx.push_back(q);
+    // two passes (count, then fill) so every point is independent: the lists
+    // and reports are exactly the sequential ones (pointcloud.cpp:257-299)
+    const int n = c.n;
+    auto in_slot = [&](int p, int q, int slot) {
+        const double dx = c.x[q] - c.x[p];
+        const double dy = c.y[q] - c.y[p];
+        switch (slot) {
+            case kXpos: return dx >= 0.0;
+            case kXneg: return dx <= 0.0;
+            case kYpos: return dy >= 0.0;
+            default: return dy <= 0.0;
         }
+    };
+    for (int sl = 0; sl < 4; ++sl) {
+        Csr& s = c.split[sl];
+        s.off.assign(n + 1, 0);
+#pragma omp parallel for schedule(static)
+        for (int p = 0; p < n; ++p) {
+            int m = 0;
+            for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1]; ++k) m += in_slot(p, c.nbr.idx[k], sl);
+            s.off[p + 1] = m;
+        }
+        for (int p = 0; p < n; ++p) s.off[p + 1] += s.off[p];
+        s.idx.assign(s.off[n], 0);
+#pragma omp parallel for schedule(static)
+        for (int p = 0; p < n; ++p) {
+            int w = s.off[p];
+            for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1]; ++k)
+                if (in_slot(p, c.nbr.idx[k], sl)) s.idx[w++] = c.nbr.idx[k];
+        }
+    }
+    std::vector<char> empty(n, 0), singular(n, 0);
+#pragma omp parallel for schedule(static)
+    for (int p = 0; p < n; ++p) {
         bool any_empty = false, any_singular = false;
         for (auto& s : c.split) {
-            s.off[p + 1] = static_cast<int>(s.idx.size());
             const int m = s.off[p + 1] - s.off[p];
             any_empty = any_empty || m == 0;
             any_singular = any_singular || report_singular(c, p, s.idx.data() + s.off[p], m);
         }
         any_singular = any_singular ||
                        report_singular(c, p, c.nbr.idx.data() + c.nbr.off[p], c.nbr.degree(p));
-        if (any_empty) c.empty_points.push_back(p);
-        if (any_singular) c.singular_points.push_back(p);
+        empty[p] = any_empty;
+        singular[p] = any_singular;
+    }
+    c.empty_points.clear();
+    c.singular_points.clear();
+    for (int p = 0; p < n; ++p) {
+        if (empty[p]) c.empty_points.push_back(p);
+        if (singular[p]) c.singular_points.push_back(p);
     }
 }
 
@@ -278,6 +304,8 @@ void ls_operators(Cloud& c)
         c.coefD[l].assign(c.n, 1.0);
     }
     c.flagged.clear();
+    std::vector<char> flags(c.n, 0);
+#pragma omp parallel for schedule(static)
     for (int p = 0; p < c.n; ++p) {
         bool flagged = false;
         const int b = c.nbr.off[p], m = c.nbr.degree(p);
@@ -314,8 +342,10 @@ void ls_operators(Cloud& c)
         split_weights(c, kXneg, true, p, flagged);
         split_weights(c, kYpos, false, p, flagged);
         split_weights(c, kYneg, false, p, flagged);
-        if (flagged) c.flagged.push_back(p);
+        flags[p] = flagged;
     }
+    for (int p = 0; p < c.n; ++p)
+        if (flags[p]) c.flagged.push_back(p);
 }
 
 // Greedy colouring over the symmetrised graph, coloring.cpp:7-52.
@@ -339,6 +369,7 @@ void greedy_colors(Cloud& c)
             adj[pos[q]++] = i;
         }
     std::vector<int> len(n);
+#pragma omp parallel for schedule(static)
     for (int i = 0; i < n; ++i) {
         int* a = adj.data() + aoff[i];
         const int m = static_cast<int>(aoff[i + 1] - aoff[i]);
@@ -405,6 +436,9 @@ struct LineScanner {
 
 void finalize(Cloud& c)
 {
+    const bool tm = std::getenv("KF_TIME_INGEST") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
     c.wall_ids.clear();
     c.interior_ids.clear();
     c.outer_ids.clear();
@@ -413,9 +447,17 @@ void finalize(Cloud& c)
         if (c.kind[i] == kInterior) c.interior_ids.push_back(i);
         if (c.kind[i] == kOuter) c.outer_ids.push_back(i);
     }
+    auto t1 = now();
     split_stencils(c);
+    auto t2 = now();
     ls_operators(c);
+    auto t3 = now();
     greedy_colors(c);
+    auto t4 = now();
+    if (tm)
+        std::fprintf(stderr, "ingest: lists %.2f split %.2f ls %.2f colour %.2f s\n",
+                     std::chrono::duration<double>(t1 - t0).count(), std::chrono::duration<double>(t2 - t1).count(),
+                     std::chrono::duration<double>(t3 - t2).count(), std::chrono::duration<double>(t4 - t3).count());
 }
 
 Cloud generate_naca_ogrid(const std::string& digits, int n_wall, int n_radial,
@@ -453,6 +495,7 @@ Cloud generate_naca_ogrid(const std::string& digits, int n_wall, int n_radial,
     for (int j = 0; j < n_radial; ++j)
         frac[j] = (std::pow(sigma, j) - 1.0) / (std::pow(sigma, n_radial - 1) - 1.0);
 
+#pragma omp parallel for schedule(static)
     for (int i = 0; i < n_wall; ++i) {
         const WallSample& s = wall[i];
         const double phi = std::atan2(s.y - cy, s.x - cx);
@@ -474,22 +517,29 @@ Cloud generate_naca_ogrid(const std::string& digits, int n_wall, int n_radial,
         }
     }
 
-    // Eight-neighbourhood, wrapped in i and clamped in j (pointcloud.cpp:237-250).
+    // Eight-neighbourhood, wrapped in i and clamped in j (pointcloud.cpp:237-250):
+    // rows 0 and n_radial-1 have 5 neighbours, the others 8, in this order
     c.nbr.off.assign(N + 1, 0);
-    c.nbr.idx.reserve(N * 8);
+    for (long id = 0; id < N; ++id) {
+        const int j = static_cast<int>(id / n_wall);
+        c.nbr.off[id + 1] = c.nbr.off[id] + ((j == 0 || j == n_radial - 1) ? 5 : 8);
+    }
+    if (n_radial == 1) throw IngestError(1, "degenerate O-grid");
+    c.nbr.idx.assign(c.nbr.off[N], 0);
+#pragma omp parallel for schedule(static)
     for (int j = 0; j < n_radial; ++j) {
         for (int i = 0; i < n_wall; ++i) {
             const long id = static_cast<long>(j) * n_wall + i;
+            int w = c.nbr.off[id];
             for (int dj = -1; dj <= 1; ++dj) {
                 const int jj = j + dj;
                 if (jj < 0 || jj >= n_radial) continue;
                 for (int di = -1; di <= 1; ++di) {
                     if (di == 0 && dj == 0) continue;
                     const int ii = (i + di + n_wall) % n_wall;
-                    c.nbr.idx.push_back(jj * n_wall + ii);
+                    c.nbr.idx[w++] = jj * n_wall + ii;
                 }
             }
-            c.nbr.off[id + 1] = static_cast<int>(c.nbr.idx.size());
         }
     }
     finalize(c);

@@ -368,10 +368,17 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
     else
         for (int r = 0; r < n_rows; ++r) ranks.push_back(r);
     parts.resize(ranks.size());
+    const bool tm = std::getenv("KF_TIME_INGEST") != nullptr;
     for (size_t k = 0; k < ranks.size(); ++k) {
+        const auto t0 = std::chrono::steady_clock::now();
         const LocalLayout L = build_local_layout(c, owner, n_rows, ranks[k], cfg.ordering);
+        const auto t1 = std::chrono::steady_clock::now();
         parts[k].rank = ranks[k];
         pack(c, L, code, oty, otx, red_shared, parts[k]);
+        if (tm)
+            std::fprintf(stderr, "partition %d: layout %.2f s, pack %.2f s\n", ranks[k],
+                         std::chrono::duration<double>(t1 - t0).count(),
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count());
     }
     if (transport == kNccl) {
         ncclUniqueId id;
@@ -500,6 +507,14 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                         const std::vector<double>& oty, const std::vector<double>& otx,
                         double* red_shared, Part& P)
 {
+    const bool tm = std::getenv("KF_TIME_INGEST") != nullptr;
+    auto tlast = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!tm) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  pack %-14s %.2f s\n", what, std::chrono::duration<double>(t - tlast).count());
+        tlast = t;
+    };
     // ---- renumbering: colour-major, owned then ghosts per colour, padded to warps
     P.gs = L.gs;
     P.oe = L.oe;
@@ -526,6 +541,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         }
     }
 
+    lap("renumber");
     // ---- per-point static data
     std::vector<int> orig(P.perm);
     std::vector<signed char> kind(n_pad, -1);
@@ -560,10 +576,28 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     std::vector<double2> lsfd(n_pad, make_double2(1, 1)), xy(n_pad, make_double2(0, 0));
     auto form = [](double A, double B, double Dn, double u, double v) { return (A * u - B * v) / Dn; };
     std::vector<unsigned char> emask(c.nbr.idx.size(), 0);  // split mask per nbr entry
-    std::vector<double4> ew(c.nbr.idx.size(), make_double4(0, 0, 0, 0));  // split weights per entry (device order)
+    // split weight of direction d (device order) of nbr entry k of global
+    // point o: the linear form, bitwise the reference's weight (checked below)
+    auto entry_w = [&](int o, int k, int d) {
+        const int i = c.nbr.idx[k];
+        const double dx = c.x[i] - c.x[o], dy = c.y[i] - c.y[o];
+        const int l = 2 + slot_of[d];
+        return d < 2 ? form(c.coefA[l][o], c.coefB[l][o], c.coefD[l][o], dx, dy)
+                     : form(c.coefA[l][o], c.coefB[l][o], c.coefD[l][o], dy, dx);
+    };
     std::vector<int> wall_slot_of(c.n, -1);
     for (int k = 0; k < W && W >= 3; ++k) wall_slot_of[c.wall_ids[k]] = k;
-    P.nnz_w = 0;
+    long long nnz_w_acc = 0;
+    std::string pack_error;  // first error of the parallel loop (thrown after it)
+    int pack_error_at = std::numeric_limits<int>::max();
+    auto fail = [&](int pn, const std::string& m) {
+#pragma omp critical(kf_pack_error)
+        if (pn < pack_error_at) {
+            pack_error_at = pn;
+            pack_error = m;
+        }
+    };
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : nnz_w_acc)
     for (int pn = 0; pn < n_pad; ++pn) {
         const int o = P.perm[pn];
         if (o < 0) continue;
@@ -608,7 +642,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             // the linear forms must reproduce the stored weights bit for bit
             if (form(c.coefA[0][o], c.coefB[0][o], c.coefD[0][o], dx, dy) != c.wx[k] ||
                 form(c.coefA[1][o], c.coefB[1][o], c.coefD[1][o], dy, dx) != c.wy[k])
-                throw SolverError(KF_RUNTIME, "LS linear form does not reproduce the full-stencil weight");
+                fail(pn, "LS linear form does not reproduce the full-stencil weight");
             // the split-list entries that this full-stencil entry became
             // (pointcloud.cpp:281-289 appends in nbr order)
             const bool in[4] = {dx >= 0.0, dx <= 0.0, dy >= 0.0, dy <= 0.0};  // slot order
@@ -616,8 +650,10 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             for (int sidx = 0; sidx < 4; ++sidx) {
                 if (!in[sidx]) continue;
                 const int pos = c.split[sidx].off[o] + cnt[sidx]++;
-                if (c.split[sidx].idx[pos] != i)
-                    throw SolverError(KF_RUNTIME, "split stencil / neighbour order mismatch");
+                if (c.split[sidx].idx[pos] != i) {
+                    fail(pn, "split stencil / neighbour order mismatch");
+                    break;
+                }
                 w[sidx] = c.split_w[sidx][pos];
             }
             unsigned mask = 0;
@@ -626,28 +662,32 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                 if (wd == 0.0) continue;
                 mask |= 1u << d;
                 const double f = d < 2 ? form(cA[d], cB[d], cD[d], dx, dy) : form(cA[d], cB[d], cD[d], dy, dx);
-                if (f != wd)
-                    throw SolverError(KF_RUNTIME, "LS linear form does not reproduce a split weight");
+                if (f != wd) fail(pn, "LS linear form does not reproduce a split weight");
             }
-            if (inv[i] < 0) throw SolverError(KF_RUNTIME, "partition layout misses a neighbour");
+            if (inv[i] < 0) {
+                fail(pn, "partition layout misses a neighbour");
+                continue;
+            }
             const int kk = k - c.nbr.off[o];
             const size_t e = static_cast<size_t>(slice_off[pn >> 5]) + 32 * kk + (pn & 31);
             e_id[e] = static_cast<unsigned>(inv[i]) | (mask << 28);
             emask[k] = static_cast<unsigned char>(mask);
-            ew[k] = make_double4(w[slot_of[0]], w[slot_of[1]], w[slot_of[2]], w[slot_of[3]]);
-            P.nnz_w += __builtin_popcount(mask);
+            nnz_w_acc += __builtin_popcount(mask);
         }
         hmin[pn] = h;
         if (c.kind[o] == kOuter && best >= 0) {
             // the planner keeps every outer point with its BC source
             // (partition.cpp), so the source is always a local owned point
             if (inv[best] < 0 || P.ghost[inv[best]])
-                throw SolverError(KF_RUNTIME, "outer BC source of point " + std::to_string(o) +
-                                                  " is not owned by its partition");
-            near_int[pn] = inv[best];
+                fail(pn, "outer BC source of point " + std::to_string(o) + " is not owned by its partition");
+            else
+                near_int[pn] = inv[best];
         }
         if (c.kind[o] == kWall) wslot[pn] = wall_slot_of[o];
     }
+    if (!pack_error.empty()) throw SolverError(KF_RUNTIME, pack_error);
+    P.nnz_w = nnz_w_acc;
+    lap("static+stencil");
     // sweep weight streams: for every owned point, the split weights the
     // forward sweep consumes (neighbours of a lower colour, nonzero weight)
     // and those the backward sweep consumes (higher colour), each in
@@ -660,35 +700,49 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         for (int g = 0; g < C; ++g)
             for (int pn = P.gs[g]; pn < P.ge[g]; ++pn) colour_of[pn] = g;
         for (int dir = 0; dir < 2; ++dir) {
+            // pass 1: per-slice width (max consumed weights of a lane)
+            auto consumed = [&](int pn, int k) {
+                const int g = colour_of[pn];
+                const int i = inv[c.nbr.idx[k]];
+                return emask[k] && (dir == 0 ? i < P.gs[g] : i >= P.ge[g]);
+            };
             swoff[dir].assign(n_slices + 1, 0);
-            std::vector<std::vector<double>> lane(32);
+#pragma omp parallel for schedule(static)
             for (int sl = 0; sl < n_slices; ++sl) {
-                size_t w = 0;
+                int w = 0;
                 for (int l = 0; l < 32; ++l) {
-                    lane[l].clear();
                     const int pn = sl * 32 + l;
                     const int o = P.perm[pn];
                     if (o < 0 || P.ghost[pn]) continue;
-                    const int g = colour_of[pn];
-                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
-                        const int i = inv[c.nbr.idx[k]];
-                        const bool use = dir == 0 ? i < P.gs[g] : i >= P.ge[g];
-                        if (!use || !emask[k]) continue;
-                        const double4 w4 = ew[k];
-                        const double wd[4] = {w4.x, w4.y, w4.z, w4.w};
-                        for (int d = 0; d < 4; ++d)
-                            if (emask[k] >> d & 1u) lane[l].push_back(wd[d]);
-                    }
-                    w = std::max(w, lane[l].size());
+                    int cnt = 0;
+                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k)
+                        if (consumed(pn, k)) cnt += __builtin_popcount(emask[k]);
+                    w = std::max(w, cnt);
                 }
-                const size_t base = swv[dir].size();
-                swv[dir].resize(base + 32 * w, 0.0);
-                for (int l = 0; l < 32; ++l)
-                    for (size_t j = 0; j < lane[l].size(); ++j) swv[dir][base + 32 * j + l] = lane[l][j];
-                swoff[dir][sl + 1] = static_cast<int>(swv[dir].size());
+                swoff[dir][sl + 1] = 32 * w;
             }
+            for (int sl = 0; sl < n_slices; ++sl) swoff[dir][sl + 1] += swoff[dir][sl];
+            swv[dir].assign(static_cast<size_t>(swoff[dir][n_slices]), 0.0);
+            // pass 2: fill in consumption order (column, then direction)
+#pragma omp parallel for schedule(static)
+            for (int sl = 0; sl < n_slices; ++sl)
+                for (int l = 0; l < 32; ++l) {
+                    const int pn = sl * 32 + l;
+                    const int o = P.perm[pn];
+                    if (o < 0 || P.ghost[pn]) continue;
+                    size_t j = static_cast<size_t>(swoff[dir][sl]) + l;
+                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
+                        if (!consumed(pn, k)) continue;
+                        for (int d = 0; d < 4; ++d)
+                            if (emask[k] >> d & 1u) {
+                                swv[dir][j] = entry_w(o, k, d);
+                                j += 32;
+                            }
+                    }
+                }
         }
     }
+    lap("sweep weights");
     // processing order of the point-parallel kernels: owned slices sorted by
     // the Morton code of their first point, so the resident front of a launch
     // is spatially compact across all colours (L2 reuse of the gathers)
@@ -707,9 +761,14 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             for (int k = 0; k < kThreads / 32; ++k) tiles.push_back(-1);
     }
 
-    // ---- SMEM-staged tiles of the gradient / residual kernels: owned points
-    // in Morton order, greedily cut into tiles of <= kTile points whose
-    // staged set (own points + their stencil neighbours) stays <= kHaloCap
+    lap("slice order");
+    // ---- SMEM-staged tiles of the gradient / residual kernels. Formation
+    // (sequential): breadth-first over the stencil graph from the first free
+    // point in Morton order (compact tiles: staged/own ~1.5 on an O-grid
+    // instead of ~1.9 for Morton chunks), topped up from the next free seeds
+    // when a region runs out, each tile <= kTile points and <= kHaloCap
+    // staged records; KF_TILE_ORDER=morton = plain Morton chunks. Content
+    // (parallel over tiles): slots, 16-bit entries, weight stream.
     std::vector<int> tpts, thoff(1, 0), thalo, teoff(1, 0);
     std::vector<unsigned short> tell;
     std::vector<double> tw;                  // streamed split weights (residual)
@@ -724,184 +783,243 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         for (int pn = 0; pn < n_pad; ++pn)
             if (P.perm[pn] >= 0 && !P.ghost[pn]) own.push_back(pn);
         std::stable_sort(own.begin(), own.end(), [&](int a, int b) { return code[P.perm[a]] < code[P.perm[b]]; });
-        std::vector<int> stamp(n_pad, -1), sstamp(n_pad, -1), slot(n_pad, -1);
-        // tile growth: breadth-first over the stencil graph from the first
-        // free point in Morton order (compact tiles: staged/own ~1.5 on an
-        // O-grid instead of ~1.9 for Morton chunks), topped up from the next
-        // free seeds when a region runs out; KF_TILE_ORDER=morton = chunks
         const char* to = std::getenv("KF_TILE_ORDER");
         const bool bfs = !(to && std::string(to) == "morton");
-        std::vector<char> taken(n_pad, 0);
-        std::vector<int> qstamp(n_pad, -1), fifo;
-        size_t seed = 0;
-        int tcount = 0;
-        std::vector<int> pts, added;
-        auto next_seed = [&]() {
-            while (seed < own.size() && taken[own[seed]]) ++seed;
-            return seed < own.size() ? own[seed] : -1;
-        };
-        while (next_seed() >= 0) {
-            pts.clear();
-            int hcount = 0;
-            fifo.clear();
-            size_t head = 0;
-            bool full = false;
-            while (!full && static_cast<int>(pts.size()) < kTile) {
-                if (head == fifo.size()) {  // region exhausted (or start): next seed
-                    const int sd = next_seed();
-                    if (sd < 0) break;
-                    qstamp[sd] = tcount;
-                    fifo.push_back(sd);
-                }
-                const int pn = fifo[head++];
-                if (taken[pn]) continue;
-                const int o = P.perm[pn];
-                added.clear();
-                auto touch = [&](int id) {
-                    if (stamp[id] != tcount) {
-                        stamp[id] = tcount;
-                        added.push_back(id);
+        // -- formation
+        std::vector<int> tile_pts, tile_off(1, 0);
+        tile_pts.reserve(own.size());
+        {
+            std::vector<int> stamp(n_pad, -1), qstamp(n_pad, -1), fifo, added;
+            std::vector<char> taken(n_pad, 0);
+            size_t seed = 0;
+            int tcount = 0;
+            auto next_seed = [&]() {
+                while (seed < own.size() && taken[own[seed]]) ++seed;
+                return seed < own.size() ? own[seed] : -1;
+            };
+            while (next_seed() >= 0) {
+                int npts = 0, hcount = 0;
+                fifo.clear();
+                size_t head = 0;
+                while (npts < kTile) {
+                    if (head == fifo.size()) {  // region exhausted (or start): next seed
+                        const int sd = next_seed();
+                        if (sd < 0) break;
+                        qstamp[sd] = tcount;
+                        fifo.push_back(sd);
                     }
-                };
-                touch(pn);
-                for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) touch(inv[c.nbr.idx[k]]);
-                if (hcount + static_cast<int>(added.size()) > halo_cap && !pts.empty()) {
-                    for (int id : added) stamp[id] = -1;
-                    full = true;
-                    break;
-                }
-                hcount += static_cast<int>(added.size());
-                pts.push_back(pn);
-                taken[pn] = 1;
-                if (!bfs) {
-                    ++seed;  // Morton chunks: the next point in order
-                    continue;
-                }
-                for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
-                    const int li = inv[c.nbr.idx[k]];
-                    if (li >= 0 && !P.ghost[li] && !taken[li] && qstamp[li] != tcount) {
-                        qstamp[li] = tcount;
-                        fifo.push_back(li);
+                    const int pn = fifo[head++];
+                    if (taken[pn]) continue;
+                    const int o = P.perm[pn];
+                    added.clear();
+                    auto touch = [&](int id) {
+                        if (stamp[id] != tcount) {
+                            stamp[id] = tcount;
+                            added.push_back(id);
+                        }
+                    };
+                    touch(pn);
+                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) touch(inv[c.nbr.idx[k]]);
+                    if (hcount + static_cast<int>(added.size()) > halo_cap && npts > 0) {
+                        for (int id : added) stamp[id] = -1;
+                        break;
                     }
-                }
-            }
-            if (hcount + 8 * 64 > 4095) throw SolverError(KF_CONFIG, "stencil too large for a 12-bit tile slot");
-            // slots: own points first (slot = lane); every halo record gets a
-            // bank class (slot mod 8), chosen greedily so that the 8 lanes of
-            // a quarter-warp reading one stencil column touch distinct 16-B
-            // bank groups (the LDS.128 reads of k_grad_t / k_residual_t);
-            // unused slots of the class grid stage a dummy record
-            const int m = static_cast<int>(pts.size());
-            int W = 0;
-            for (int pn : pts) W = std::max(W, c.nbr.degree(P.perm[pn]));
-            P.w_max = std::max(P.w_max, W);
-            for (int t = 0; t < m; ++t) {
-                sstamp[pts[t]] = tcount;
-                slot[pts[t]] = t;
-            }
-            std::vector<int> hid;                     // halo records, first-use order
-            std::vector<std::vector<int>> hgroups;    // their (column, quarter-warp) groups
-            std::vector<unsigned char> gmask(static_cast<size_t>(W) * (kTile / 8), 0);
-            for (int t = 0; t < m; ++t) {
-                const int o = P.perm[pts[t]];
-                for (int kk = 0; kk < c.nbr.degree(o); ++kk) {
-                    const int id = inv[c.nbr.idx[c.nbr.off[o] + kk]];
-                    const int g = kk * (kTile / 8) + (t >> 3);
-                    if (sstamp[id] == tcount && slot[id] >= 0 && slot[id] < m) {  // own point
-                        gmask[g] |= static_cast<unsigned char>(1u << (slot[id] & 7));
+                    hcount += static_cast<int>(added.size());
+                    tile_pts.push_back(pn);
+                    ++npts;
+                    taken[pn] = 1;
+                    if (!bfs) {
+                        ++seed;
                         continue;
                     }
-                    if (sstamp[id] != tcount) {
-                        sstamp[id] = tcount;
-                        slot[id] = -1 - static_cast<int>(hid.size());  // halo index, encoded
-                        hid.push_back(id);
-                        hgroups.emplace_back();
-                    }
-                    std::vector<int>& hg = hgroups[-1 - slot[id]];
-                    if (hg.empty() || hg.back() != g) hg.push_back(g);
-                }
-            }
-            const int base = (m + 7) & ~7;
-            int cls_count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            std::vector<int> hslot(hid.size());
-            int ns = m;
-            for (size_t h = 0; h < hid.size(); ++h) {
-                int best = 0, best_cost = 1 << 30;
-                for (int b = 0; b < 8; ++b) {
-                    int cost = 0;
-                    for (int g : hgroups[h]) cost += (gmask[g] >> b) & 1;
-                    cost = cost * 4096 + cls_count[b];
-                    if (cost < best_cost) {
-                        best_cost = cost;
-                        best = b;
-                    }
-                }
-                for (int g : hgroups[h]) gmask[g] |= static_cast<unsigned char>(1u << best);
-                hslot[h] = base + 8 * cls_count[best] + best;
-                ++cls_count[best];
-                ns = std::max(ns, hslot[h] + 1);
-            }
-            if (ns > 4096) throw SolverError(KF_CONFIG, "tile slots exceed the 12-bit entry field");
-            {
-                const size_t t0 = thalo.size();
-                thalo.resize(t0 + ns, P.perm[pts[0]] >= 0 ? pts[0] : 0);
-                for (int t = 0; t < m; ++t) thalo[t0 + t] = pts[t];
-                for (size_t h = 0; h < hid.size(); ++h) {
-                    thalo[t0 + hslot[h]] = hid[h];
-                    slot[hid[h]] = hslot[h];
-                }
-            }
-            std::vector<unsigned short> ent(static_cast<size_t>(W) * kTile, 0);
-            for (int t = 0; t < m; ++t) {
-                const int o = P.perm[pts[t]];
-                const int deg = c.nbr.degree(o);
-                for (int kk = 0; kk < W; ++kk) {
-                    unsigned e = static_cast<unsigned>(t);  // padding: self, no split
-                    if (kk < deg) {
-                        const int k = c.nbr.off[o] + kk;
-                        e = static_cast<unsigned>(slot[inv[c.nbr.idx[k]]]) | (unsigned(emask[k]) << 12);
-                    }
-                    ent[static_cast<size_t>(kk) * kTile + t] = static_cast<unsigned short>(e);
-                }
-            }
-            tell.insert(tell.end(), ent.begin(), ent.end());
-            teoff.push_back(static_cast<int>(tell.size()));
-            // the nonzero split weights of each lane in consumption order
-            // (column, then direction), column-major over the tile
-            {
-                std::vector<std::vector<double>> lw(pts.size());
-                size_t ww = 0;
-                for (size_t t = 0; t < pts.size(); ++t) {
-                    const int o = P.perm[pts[t]];
                     for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
-                        const double4 w4 = ew[k];
-                        const double wd[4] = {w4.x, w4.y, w4.z, w4.w};
-                        for (int d = 0; d < 4; ++d)
-                            if (emask[k] >> d & 1u) lw[t].push_back(wd[d]);
+                        const int li = inv[c.nbr.idx[k]];
+                        if (li >= 0 && !P.ghost[li] && !taken[li] && qstamp[li] != tcount) {
+                            qstamp[li] = tcount;
+                            fifo.push_back(li);
+                        }
                     }
-                    ww = std::max(ww, lw[t].size());
                 }
-                const size_t base = tw.size();
-                tw.resize(base + ww * kTile, 0.0);
-                for (size_t t = 0; t < pts.size(); ++t)
-                    for (size_t j = 0; j < lw[t].size(); ++j) tw[base + j * kTile + t] = lw[t][j];
-                twoff.push_back(static_cast<long long>(tw.size()));
+                tile_off.push_back(static_cast<int>(tile_pts.size()));
+                ++tcount;
             }
-            thoff.push_back(static_cast<int>(thalo.size()));
-            nh_max = std::max(nh_max, ns);
-            for (int t = 0; t < kTile; ++t) {
-                const bool real = t < static_cast<int>(pts.size());
-                const int pn = real ? pts[t] : 0;
-                tpts.push_back(real ? pn : -1);
-                tlsf.push_back(real ? lsf[pn] : make_double4(0, 0, 0, 0));
-                tlsfd.push_back(real ? lsfd[pn] : make_double2(1, 1));
-                tlsA.push_back(real ? lsA[pn] : make_double4(0, 0, 0, 0));
-                tlsB.push_back(real ? lsB[pn] : make_double4(0, 0, 0, 0));
-                tlsD.push_back(real ? lsD[pn] : make_double4(1, 1, 1, 1));
-            }
-            ++tcount;
         }
-        if (tcount == 0) {  // empty partition: one idle tile
+        const int n_tiles = static_cast<int>(tile_off.size()) - 1;
+        // -- content, one tile per task
+        struct TileOut {
+            std::vector<int> halo;
+            std::vector<unsigned short> ent;
+            std::vector<double> w;
+            int W = 0, ns = 0;
+        };
+        std::vector<TileOut> outs(std::max(n_tiles, 0));
+        std::string tile_error;
+#pragma omp parallel
+        {
+            // per-thread scratch: open-addressing map local id -> index
+            constexpr int kH = 8192;
+            std::vector<int> hkey(kH, -1), hval(kH, 0), used;
+            auto find = [&](int key) -> int& {
+                unsigned h = (static_cast<unsigned>(key) * 2654435761u) & (kH - 1);
+                while (hkey[h] != -1 && hkey[h] != key) h = (h + 1) & (kH - 1);
+                if (hkey[h] == -1) {
+                    hkey[h] = key;
+                    hval[h] = -1;
+                    used.push_back(static_cast<int>(h));
+                }
+                return hval[h];
+            };
+            std::vector<int> hid, pair_h, pair_g, order, hstart;
+            std::vector<unsigned char> gmask;
+            std::vector<int> refslot;
+#pragma omp for schedule(dynamic, 16)
+            for (int ti = 0; ti < n_tiles; ++ti) {
+                TileOut& O = outs[ti];
+                const int* pts = tile_pts.data() + tile_off[ti];
+                const int m = tile_off[ti + 1] - tile_off[ti];
+                for (int u : used) hkey[u] = -1;
+                used.clear();
+                int W = 0;
+                for (int t = 0; t < m; ++t) W = std::max(W, c.nbr.degree(P.perm[pts[t]]));
+                for (int t = 0; t < m; ++t) find(pts[t]) = t;  // own points: slot = lane
+                // halo records in first-use order with their (column,
+                // quarter-warp) groups; own reads mark their bank class
+                hid.clear();
+                pair_h.clear();
+                pair_g.clear();
+                gmask.assign(static_cast<size_t>(W) * (kTile / 8), 0);
+                for (int t = 0; t < m; ++t) {
+                    const int o = P.perm[pts[t]];
+                    for (int kk = 0; kk < c.nbr.degree(o); ++kk) {
+                        const int id = inv[c.nbr.idx[c.nbr.off[o] + kk]];
+                        const int g = kk * (kTile / 8) + (t >> 3);
+                        int& v = find(id);
+                        if (v >= 0 && v < m) {  // own point
+                            gmask[g] |= static_cast<unsigned char>(1u << (v & 7));
+                            continue;
+                        }
+                        if (v == -1) {
+                            v = -2 - static_cast<int>(hid.size());  // halo index, encoded
+                            hid.push_back(id);
+                        }
+                        pair_h.push_back(-2 - v);
+                        pair_g.push_back(g);
+                    }
+                }
+                // groups of each halo record (counting sort keeps first-use order)
+                const int nh = static_cast<int>(hid.size());
+                hstart.assign(nh + 1, 0);
+                for (int h : pair_h) ++hstart[h + 1];
+                for (int h = 0; h < nh; ++h) hstart[h + 1] += hstart[h];
+                order.assign(pair_h.size(), 0);
+                {
+                    std::vector<int> fill(hstart.begin(), hstart.end() - 1);
+                    for (size_t q = 0; q < pair_h.size(); ++q) order[fill[pair_h[q]]++] = pair_g[q];
+                }
+                const int base = (m + 7) & ~7;
+                int cls_count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                int ns = m;
+                std::vector<int> hslot(nh);
+                for (int h = 0; h < nh; ++h) {
+                    int best = 0, best_cost = 1 << 30;
+                    for (int b = 0; b < 8; ++b) {
+                        int cost = 0;
+                        for (int q = hstart[h]; q < hstart[h + 1]; ++q) cost += (gmask[order[q]] >> b) & 1;
+                        cost = cost * 4096 + cls_count[b];
+                        if (cost < best_cost) {
+                            best_cost = cost;
+                            best = b;
+                        }
+                    }
+                    for (int q = hstart[h]; q < hstart[h + 1]; ++q) gmask[order[q]] |= static_cast<unsigned char>(1u << best);
+                    hslot[h] = base + 8 * cls_count[best] + best;
+                    ++cls_count[best];
+                    ns = std::max(ns, hslot[h] + 1);
+                }
+                if (ns > 4096) {
+#pragma omp critical(kf_tile_error)
+                    tile_error = "tile slots exceed the 12-bit entry field";
+                    continue;
+                }
+                O.W = W;
+                O.ns = ns;
+                O.halo.assign(ns, pts[0]);  // unused class-grid slots stage a dummy record
+                for (int t = 0; t < m; ++t) O.halo[t] = pts[t];
+                for (int h = 0; h < nh; ++h) O.halo[hslot[h]] = hid[h];
+                O.ent.assign(static_cast<size_t>(W) * kTile, 0);
+                for (int t = 0; t < m; ++t) {
+                    const int o = P.perm[pts[t]];
+                    const int deg = c.nbr.degree(o);
+                    for (int kk = 0; kk < W; ++kk) {
+                        unsigned e = static_cast<unsigned>(t);  // padding: self, no split
+                        if (kk < deg) {
+                            const int k = c.nbr.off[o] + kk;
+                            const int v = find(inv[c.nbr.idx[k]]);
+                            const int sl = v >= 0 ? v : hslot[-2 - v];
+                            e = static_cast<unsigned>(sl) | (unsigned(emask[k]) << 12);
+                        }
+                        O.ent[static_cast<size_t>(kk) * kTile + t] = static_cast<unsigned short>(e);
+                    }
+                }
+                // the nonzero split weights of each lane in consumption order
+                // (column, then direction), column-major over the tile
+                int ww = 0;
+                for (int t = 0; t < m; ++t) {
+                    const int o = P.perm[pts[t]];
+                    int cnt = 0;
+                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) cnt += __builtin_popcount(emask[k]);
+                    ww = std::max(ww, cnt);
+                }
+                O.w.assign(static_cast<size_t>(ww) * kTile, 0.0);
+                for (int t = 0; t < m; ++t) {
+                    const int o = P.perm[pts[t]];
+                    size_t j = t;
+                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k)
+                        for (int d = 0; d < 4; ++d)
+                            if (emask[k] >> d & 1u) {
+                                O.w[j] = entry_w(o, k, d);
+                                j += kTile;
+                            }
+                }
+            }
+        }
+        if (!tile_error.empty()) throw SolverError(KF_CONFIG, tile_error);
+        // -- concatenate
+        for (int ti = 0; ti < n_tiles; ++ti) {
+            thoff.push_back(thoff.back() + outs[ti].ns);
+            teoff.push_back(teoff.back() + static_cast<int>(outs[ti].ent.size()));
+            twoff.push_back(twoff.back() + static_cast<long long>(outs[ti].w.size()));
+            nh_max = std::max(nh_max, outs[ti].ns);
+            P.w_max = std::max(P.w_max, outs[ti].W);
+        }
+        thalo.resize(thoff.back());
+        tell.resize(teoff.back());
+        tw.resize(twoff.back());
+        tpts.assign(static_cast<size_t>(n_tiles) * kTile, -1);
+        tlsf.assign(tpts.size(), make_double4(0, 0, 0, 0));
+        tlsfd.assign(tpts.size(), make_double2(1, 1));
+        tlsA.assign(tpts.size(), make_double4(0, 0, 0, 0));
+        tlsB.assign(tpts.size(), make_double4(0, 0, 0, 0));
+        tlsD.assign(tpts.size(), make_double4(1, 1, 1, 1));
+#pragma omp parallel for schedule(static)
+        for (int ti = 0; ti < n_tiles; ++ti) {
+            std::copy(outs[ti].halo.begin(), outs[ti].halo.end(), thalo.begin() + thoff[ti]);
+            std::copy(outs[ti].ent.begin(), outs[ti].ent.end(), tell.begin() + teoff[ti]);
+            std::copy(outs[ti].w.begin(), outs[ti].w.end(), tw.begin() + twoff[ti]);
+            const int m = tile_off[ti + 1] - tile_off[ti];
+            for (int t = 0; t < m; ++t) {
+                const int pn = tile_pts[tile_off[ti] + t];
+                const size_t q = static_cast<size_t>(ti) * kTile + t;
+                tpts[q] = pn;
+                tlsf[q] = lsf[pn];
+                tlsfd[q] = lsfd[pn];
+                tlsA[q] = lsA[pn];
+                tlsB[q] = lsB[pn];
+                tlsD[q] = lsD[pn];
+            }
+        }
+        P.n_tiles = n_tiles;
+        if (n_tiles == 0) {  // empty partition: one idle tile
             tpts.assign(kTile, -1);
             tlsf.assign(kTile, make_double4(0, 0, 0, 0));
             tlsfd.assign(kTile, make_double2(1, 1));
@@ -914,10 +1032,10 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             tell.push_back(0);
             twoff.push_back(0);
             tw.push_back(0.0);
-            tcount = 1;
+            P.n_tiles = 1;
         }
-        P.n_tiles = tcount;
     }
+    lap("tiles");
     P.nh_cap = nh_max | 1;  // odd: SoA field rows start on different banks
 
     // ---- halo plan (send list colour-major, peer-minor)
@@ -940,6 +1058,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     P.cstart[C] = static_cast<int>(send_list.size());
     P.n_send = static_cast<int>(send_list.size());
 
+    lap("halo plan");
     // ---- device buffers
     Dev& D = P.D;
     auto up = [&](auto* d, const auto& h) { h2d(d, h.data(), h.size(), s); };
@@ -1159,6 +1278,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     }
     P.Usnap = dalloc<double4>(n_pad, owned);
     P.dUsnap = dalloc<double4>(n_pad, owned);
+    lap("upload");
     ck(cudaStreamSynchronize(s), "pack sync");
 }
 
