@@ -275,6 +275,9 @@ def main():
                     help="run a few steps for ncu (no JSON line)")
     ap.add_argument("--points", default=None, help="override cloud n_wall:n_radial")
     ap.add_argument("--parts", type=int, default=1, help="in-process partitions on one GPU")
+    ap.add_argument("--variant", default=None,
+                    choices=["explicit", "anandh", "anandh_ad", "manish", "manish_ad"],
+                    help="override the case's solver variant (evidence runs)")
     ap.add_argument("--case", type=int, default=2, choices=sorted(CASES),
                     help="BASELINE.json config whose cloud/case to time (default 2, the bench workload)")
     args = ap.parse_args()
@@ -292,6 +295,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = case_for(world, args.points, args.case)
+    if args.variant:
+        spec["variant"] = args.variant
 
     cloud = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
     N = cloud.n()
