@@ -255,6 +255,7 @@ struct Solver::Impl {
     // neighbour gathers of the gradient / residual kernels: 1 SMEM-staged
     // tiles (default), 0 global-gather sliced ELL (A/B reference)
     int gather = 1;
+    int fused_tail = 0;  // KF_FUSED_TAIL=1: k_update_fin (update + finalize in one launch)
     void launch_grad(Part& P, bool first, int src, int dst)
     {
         if (gather) {
@@ -346,6 +347,8 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // A/B switch for the neighbour gathers of the gradient/residual kernels
         const char* g = std::getenv("KF_GATHER");
         gather = (g && std::string(g) == "ell") ? 0 : 1;
+        const char* ft = std::getenv("KF_FUSED_TAIL");
+        fused_tail = ft && std::string(ft) == "1";
     }
     std::vector<double> oty, otx;
     setup_globals(c, oty, otx);
@@ -1206,6 +1209,11 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     ck(cudaMemsetAsync(D.fb_part, 0, sizeof(int), s), "memset");
     D.n_res_blocks = gather ? P.n_tiles : P.n_tile_blocks;  // blocks of the residual launch
     D.status = dalloc<unsigned long long>(1, owned);
+    {
+        unsigned* t = dalloc<unsigned>(1, owned);
+        ck(cudaMemsetAsync(t, 0, sizeof(unsigned), s), "memset");
+        D.ticket = t;
+    }
     D.iter = dalloc<int>(1, owned);
     D.nrec = dalloc<int>(1, owned);
     D.res0 = dalloc<double>(1, owned);
@@ -1447,6 +1455,11 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
             }
             if (halo && c > 0) exchange_j(c);
         }
+    }
+    if (!halo && fused_tail) {
+        k_update_fin<<<blocks_for(parts[0].n_pad, 256), 256, 0, s>>>(parts[0].D, cb, cfl_override);
+        mark("update_bc_q_finalize");
+        return;
     }
     for (Part& P : parts) {
         k_update<<<blocks_for(P.n_pad, 256), 256, 0, s>>>(P.D, cb, cfl_override);
@@ -1691,7 +1704,7 @@ void Solver::iterate_async(int n)
             if (I.cfg.use_graph && I.bench_graph) {
                 ck(cudaGraphLaunch(I.bench_graph, I.s), "graph launch");
             } else {
-                I.enqueue_iteration(0, 0.0, true);
+                I.enqueue_iteration(0, 0.0, false);
             }
             I.cur = 1;
         } else {
@@ -1717,7 +1730,7 @@ void Solver::bench_mode(int mode)
         const int saved = I.launches;
         cudaGraph_t g;
         ck(cudaStreamBeginCapture(I.s, cudaStreamCaptureModeThreadLocal), "capture");
-        I.enqueue_iteration(0, 0.0, true);
+        I.enqueue_iteration(0, 0.0, false);
         ck(cudaStreamEndCapture(I.s, &g), "capture end");
         cudaGraphDestroy(g);
         I.launches_bench = I.launches;
@@ -1735,7 +1748,7 @@ void Solver::bench_mode(int mode)
     if (I.cfg.use_graph && !I.bench_graph) {
         cudaGraph_t g;
         ck(cudaStreamBeginCapture(I.s, cudaStreamCaptureModeThreadLocal), "capture");
-        I.enqueue_iteration(0, 0.0, true);
+        I.enqueue_iteration(0, 0.0, false);
         I.launches_bench = I.launches;
         ck(cudaStreamEndCapture(I.s, &g), "capture end");
         ck(cudaGraphInstantiate(&I.bench_graph, g, 0), "graph instantiate");
@@ -1867,10 +1880,11 @@ int Solver::step_host(const double* U_in, const double* dU_in, double* U_out, do
         ck(cudaMemcpyAsync(P.D.iter, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
         ck(cudaMemcpyAsync(P.D.nrec, &zero, sizeof zero, cudaMemcpyHostToDevice, I.s), "H2D");
     }
+    for (Part& P : I.parts) k_q_from_u<<<blocks_for(P.n_pad, 256), 256, 0, I.s>>>(P.D, 0, 1);
     if (I.cfg.use_graph && I.bench_graph)
         ck(cudaGraphLaunch(I.bench_graph, I.s), "graph launch");
     else
-        I.enqueue_iteration(0, 0.0, true);
+        I.enqueue_iteration(0, 0.0, false);
     I.download_state(U_out, [](Part& P) { return static_cast<const double4*>(P.D.U[1]); });
     if (dU_out) I.download_state(dU_out, [](Part& P) { return static_cast<const double4*>(P.D.dU); });
     DevRecord r;
@@ -2265,7 +2279,7 @@ void Solver::profile_kernels(int reps, std::vector<std::string>& names, std::vec
         nm.clear();
         I.prof_ev = &all[r];
         I.prof_names = &nm;
-        I.enqueue_iteration(I.bench ? 0 : I.cur, 0.0, I.bench != 0);
+        I.enqueue_iteration(I.bench ? 0 : I.cur, 0.0, false);
         I.prof_ev = nullptr;
         I.prof_names = nullptr;
         if (I.bench)
