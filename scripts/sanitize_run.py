@@ -1,0 +1,20 @@
+"""A few iterations of every transport under compute-sanitizer (memcheck/racecheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2406_07441_b200 as kf
+c = kf.generate_naca_ogrid("0012", 64, 16, 12.0)
+for variant in ("manish_ad", "anandh", "explicit"):
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(variant), mach_inf=0.63, aoa_deg=2.0,
+                          cfl=0.05 if variant == "explicit" else 0.2, n_iterations=6)
+    for parts in (1, 3):
+        r = kf.Solver(c, cfg, n_parts=parts).run()
+        print(variant, parts, len(r.iters), r.abort_reason, flush=True)
+s = kf.Solver.for_rank(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD, n_iterations=4), 1, 0, kf.nccl_unique_id())
+print("nccl", len(s.run().iters))
+s = kf.Solver(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD, n_iterations=8))
+s.reset(); s.iterate_async(2); U, dU = s.get_state(with_dU=True)
+outs = [np.zeros_like(U) for _ in range(3)]
+s.step_host_batch([U] * 3, [dU] * 3, outs, [np.zeros_like(U) for _ in range(3)])
+s.bench_mode(True); s.iterate_async(2); print("bench", s.sync_records()[1].code)
+print("done")
