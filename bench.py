@@ -278,6 +278,8 @@ def main():
     ap.add_argument("--variant", default=None,
                     choices=["explicit", "anandh", "anandh_ad", "manish", "manish_ad"],
                     help="override the case's solver variant (evidence runs)")
+    ap.add_argument("--ordering", type=int, default=1, choices=[0, 1, 2],
+                    help="in-colour point order: 0 natural, 1 Morton (default), 2 reverse Cuthill-McKee")
     ap.add_argument("--case", type=int, default=2, choices=sorted(CASES),
                     help="BASELINE.json config whose cloud/case to time (default 2, the bench workload)")
     args = ap.parse_args()
@@ -301,7 +303,8 @@ def main():
     cloud = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
     N = cloud.n()
     cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(spec["variant"]), mach_inf=spec["mach"],
-                          aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=64, device=local)
+                          aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=64, device=local,
+                          ordering=args.ordering)
     if world > 1:
         ids = [kf.nccl_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(ids, src=0)

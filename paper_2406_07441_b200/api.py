@@ -327,7 +327,7 @@ class SolverConfig:
     cfl_start: float = 0.0
     divergence_factor: float = 1e6
     device: int = 0
-    ordering: int = 1       # in-colour point order: 0 natural, 1 Morton (default)
+    ordering: int = 1       # in-colour point order: 0 natural, 1 Morton (default), 2 RCM
     use_graph: bool = True
 
     def to_c(self) -> L.Config:

@@ -42,6 +42,57 @@ std::vector<uint64_t> morton_codes(const Cloud& c)
     return code;
 }
 
+std::vector<int> rcm_rank(const Cloud& c)
+{
+    // reverse Cuthill-McKee over the symmetrised stencil graph: breadth-first
+    // from a minimum-degree start of every component, neighbours visited in
+    // ascending degree (ties: id), the whole visit order reversed
+    const int n = c.n;
+    std::vector<int> deg(n, 0);
+    for (int p = 0; p < n; ++p)
+        for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1]; ++k) {
+            ++deg[p];
+            ++deg[c.nbr.idx[k]];
+        }
+    std::vector<long> off(n + 1, 0);
+    for (int p = 0; p < n; ++p) off[p + 1] = off[p] + deg[p];
+    std::vector<int> adj(off[n]);
+    std::vector<long> pos(off.begin(), off.end() - 1);
+    for (int p = 0; p < n; ++p)
+        for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1]; ++k) {
+            const int q = c.nbr.idx[k];
+            adj[pos[p]++] = q;
+            adj[pos[q]++] = p;
+        }
+    std::vector<int> order;
+    order.reserve(n);
+    std::vector<char> seen(n, 0);
+    std::vector<int> by_deg(n);
+    std::iota(by_deg.begin(), by_deg.end(), 0);
+    std::stable_sort(by_deg.begin(), by_deg.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+    std::vector<int> nb;
+    for (int start : by_deg) {
+        if (seen[start]) continue;
+        size_t head = order.size();
+        order.push_back(start);
+        seen[start] = 1;
+        while (head < order.size()) {
+            const int p = order[head++];
+            nb.clear();
+            for (long k = off[p]; k < off[p + 1]; ++k)
+                if (!seen[adj[k]]) {
+                    seen[adj[k]] = 1;
+                    nb.push_back(adj[k]);
+                }
+            std::sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] != deg[b] ? deg[a] < deg[b] : a < b; });
+            order.insert(order.end(), nb.begin(), nb.end());
+        }
+    }
+    std::vector<int> rank(n, 0);
+    for (int k = 0; k < n; ++k) rank[order[n - 1 - k]] = k;
+    return rank;
+}
+
 std::vector<int> bc_sources(const Cloud& c)
 {
     std::vector<int> src(c.n, -1);
@@ -140,7 +191,11 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
     std::vector<std::vector<int>> owned(C);
     for (int p = 0; p < c.n; ++p)
         if (owner[p] == rank) owned[col(p)].push_back(p);
-    if (ordering == 1) {
+    if (ordering == 2) {
+        const std::vector<int> rk = rcm_rank(c);
+        for (auto& m : owned)
+            std::stable_sort(m.begin(), m.end(), [&](int a, int b) { return rk[a] < rk[b]; });
+    } else if (ordering == 1) {
         const std::vector<uint64_t> code = morton_codes(c);
         for (auto& m : owned)
             std::stable_sort(m.begin(), m.end(), [&](int a, int b) { return code[a] < code[b]; });

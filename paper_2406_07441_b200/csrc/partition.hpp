@@ -53,7 +53,12 @@ struct LocalLayout {
     int n_owned = 0;
 };
 
-// ordering: 0 natural (ascending global id), 1 Morton over the global
+// Reverse Cuthill-McKee rank of every point (bandwidth-reducing order of the
+// symmetrised stencil graph).
+std::vector<int> rcm_rank(const Cloud& c);
+
+// ordering: 0 natural (ascending global id), 2 reverse Cuthill-McKee,
+// 1 Morton over the global
 // bounding box (the single-GPU in-colour orders).
 LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, int n_parts, int rank,
                                int ordering);

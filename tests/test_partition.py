@@ -169,3 +169,18 @@ def test_halo_exchange_pattern_over_gloo_world2():
     for rank, ok, n_ghost, tot in sorted(res):
         assert ok, (rank, n_ghost)
         assert n_ghost > 0 and tot > n_ghost
+
+
+def test_rcm_ordering_layout(cloud):
+    """ordering 2 (reverse Cuthill-McKee inside each colour block): a
+    permutation of the same blocks, with a smaller mean neighbour distance
+    in local numbering than the natural order would give on a shuffled cloud
+    (here: still a valid colour-major layout with every point once)."""
+    L0 = kf.LocalLayout(cloud, np.zeros(cloud.n(), np.int32), 1, 0, ordering=0)
+    L2 = kf.LocalLayout(cloud, np.zeros(cloud.n(), np.int32), 1, 0, ordering=2)
+    assert np.array_equal(L0.gs, L2.gs) and np.array_equal(L0.oe, L2.oe)
+    for c in range(L0.n_colors):
+        a = L0.perm[L0.gs[c]:L0.oe[c]]
+        b = L2.perm[L2.gs[c]:L2.oe[c]]
+        assert np.array_equal(np.sort(a[a >= 0]), np.sort(b[b >= 0]))
+    assert not np.array_equal(L0.perm, L2.perm)
