@@ -226,6 +226,26 @@ def time_to_drop(kf, decades=1.0, with_cpu=True):
     return out
 
 
+def shuffled(kf, c, seed=7):
+    """The same cloud under a random point numbering (kf_cloud_from_arrays
+    rebuilds split stencils, LS weights and the greedy colouring)."""
+    n = c.n()
+    # wall points keep their (surface-ordered) ids so compute_forces' loop
+    # check holds; every other point gets a random id
+    wall = np.flatnonzero(c.kind == 0)
+    rest = np.setdiff1d(np.arange(n), wall)
+    perm = np.concatenate([wall, np.random.default_rng(seed).permutation(rest)])  # new id -> old id
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    nb = c.nbr
+    deg = np.diff(nb.offsets)[perm]
+    off = np.zeros(n + 1, np.int32)
+    np.cumsum(deg, out=off[1:])
+    ids = np.concatenate([inv[nb.ids[nb.offsets[o]:nb.offsets[o + 1]]] for o in perm]).astype(np.int32)
+    return kf.PointCloud.from_arrays(c.x[perm], c.y[perm], c.kind[perm].astype(np.int32), c.normal_x[perm],
+                                     c.normal_y[perm], off, ids)
+
+
 def case_for(world, points=None, case=2):
     """The bench workload at `world` GPUs: config 2 at N=1; the cloud grows
     with N in the wall direction (weak scaling, ~640,000 points per GPU)."""
@@ -280,6 +300,9 @@ def main():
                     help="override the case's solver variant (evidence runs)")
     ap.add_argument("--ordering", type=int, default=1, choices=[0, 1, 2],
                     help="in-colour point order: 0 natural, 1 Morton (default), 2 reverse Cuthill-McKee")
+    ap.add_argument("--shuffle", action="store_true",
+                    help="randomly renumber the cloud's points first (a loaded cloud with no locality: "
+                         "the --ordering demonstration)")
     ap.add_argument("--case", type=int, default=2, choices=sorted(CASES),
                     help="BASELINE.json config whose cloud/case to time (default 2, the bench workload)")
     args = ap.parse_args()
@@ -301,6 +324,8 @@ def main():
         spec["variant"] = args.variant
 
     cloud = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
+    if args.shuffle:
+        cloud = shuffled(kf, cloud)
     N = cloud.n()
     cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(spec["variant"]), mach_inf=spec["mach"],
                           aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=64, device=local,
