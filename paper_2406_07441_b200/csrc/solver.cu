@@ -69,8 +69,8 @@ void d2h(T* h, const T* d, size_t n, cudaStream_t s)
 
 unsigned key_iter(unsigned long long k) { return static_cast<unsigned>(k >> 44); }
 int key_stage(unsigned long long k) { return static_cast<int>((k >> 36) & 0xff); }
-int key_reason(unsigned long long k) { return static_cast<int>((k >> 32) & 0xf); }
-int key_point(unsigned long long k) { return static_cast<int>(k & 0xffffffffu); }
+int key_reason(unsigned long long k) { return static_cast<int>(k & 0xf); }
+int key_point(unsigned long long k) { return static_cast<int>((k >> 4) & 0xffffffffu); }
 
 // scatter/gather between reference numbering (AoS n x 4) and device order;
 // downloads skip ghosts (kind < 0), uploads fill them too
@@ -143,6 +143,31 @@ __global__ void k_cp(Dev D, int buf)
 }
 
 int blocks_for(long n, int t) { return static_cast<int>((n + t - 1) / t); }
+
+// Capture what `enqueue` puts on `st` into an executable graph; if anything
+// throws mid-capture the capture is ended and discarded first, so the thread
+// is not left in capture mode (later allocations would fail).
+template <class F>
+cudaGraphExec_t capture_graph(cudaStream_t st, F&& enqueue)
+{
+    ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+    try {
+        enqueue();
+    } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        throw;
+    }
+    cudaGraph_t g;
+    ck(cudaStreamEndCapture(st, &g), "capture end");
+    cudaGraphExec_t x = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&x, g, 0);
+    cudaGraphDestroy(g);
+    ck(e, "graph instantiate");
+    return x;
+}
 
 enum Transport : int { kSingle = 0, kInProc = 1, kNccl = 2 };
 
@@ -1443,6 +1468,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
     if (parts[0].D.implicit) {
         for (int c = 0; c < C; ++c) {
             for (Part& P : parts) {
+                if (P.oe[c] == P.gs[c]) continue;  // no owned point of this colour here
                 k_forward<<<blocks_for(P.oe[c] - P.gs[c], T), T, 0, s>>>(P.D, cb, c, cfl_override);
                 mark("lusgs_forward");
             }
@@ -1450,6 +1476,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
         }
         for (int c = C - 2; c >= 0; --c) {
             for (Part& P : parts) {
+                if (P.oe[c] == P.gs[c]) continue;
                 k_backward<<<blocks_for(P.oe[c] - P.gs[c], T), T, 0, s>>>(P.D, cb, c);
                 mark("lusgs_backward");
             }
@@ -1484,14 +1511,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
 void Solver::Impl::build_graphs()
 {
     if (!cfg.use_graph) return;
-    for (int b = 0; b < 2; ++b) {
-        cudaGraph_t g;
-        ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
-        enqueue_iteration(b, 0.0, false);
-        ck(cudaStreamEndCapture(s, &g), "capture end");
-        ck(cudaGraphInstantiate(&graph[b], g, 0), "graph instantiate");
-        cudaGraphDestroy(g);
-    }
+    for (int b = 0; b < 2; ++b) graph[b] = capture_graph(s, [&] { enqueue_iteration(b, 0.0, false); });
 }
 
 void Solver::Impl::upload_state(const double* host, const std::function<double4*(Part&)>& sel)
@@ -1726,13 +1746,10 @@ void Solver::bench_mode(int mode)
         I.bench = 0;
         return;
     }
-    if (!I.cfg.use_graph) {
+    if (!I.cfg.use_graph) {  // count the launches of one bench step
         const int saved = I.launches;
-        cudaGraph_t g;
-        ck(cudaStreamBeginCapture(I.s, cudaStreamCaptureModeThreadLocal), "capture");
-        I.enqueue_iteration(0, 0.0, false);
-        ck(cudaStreamEndCapture(I.s, &g), "capture end");
-        cudaGraphDestroy(g);
+        cudaGraphExec_t x = capture_graph(I.s, [&] { I.enqueue_iteration(0, 0.0, false); });
+        cudaGraphExecDestroy(x);
         I.launches_bench = I.launches;
         I.launches = saved;
     }
@@ -1746,13 +1763,8 @@ void Solver::bench_mode(int mode)
     I.snap_iter = std::min(*I.h_iter, I.p0().D.rec_capacity - 1);
     I.bench = 1;
     if (I.cfg.use_graph && !I.bench_graph) {
-        cudaGraph_t g;
-        ck(cudaStreamBeginCapture(I.s, cudaStreamCaptureModeThreadLocal), "capture");
-        I.enqueue_iteration(0, 0.0, false);
+        I.bench_graph = capture_graph(I.s, [&] { I.enqueue_iteration(0, 0.0, false); });
         I.launches_bench = I.launches;
-        ck(cudaStreamEndCapture(I.s, &g), "capture end");
-        ck(cudaGraphInstantiate(&I.bench_graph, g, 0), "graph instantiate");
-        cudaGraphDestroy(g);
     }
 }
 
@@ -1921,14 +1933,7 @@ void Solver::Impl::ensure_pipe(int m)
         }
         pipe.drec = dalloc<DevRecord>(2, owned);
         pipe.dstat = dalloc<unsigned long long>(2, owned);
-        if (cfg.use_graph) {
-            cudaGraph_t g;
-            ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
-            enqueue_iteration(0, 0.0, true);
-            ck(cudaStreamEndCapture(s, &g), "capture end");
-            ck(cudaGraphInstantiate(&pipe.graph, g, 0), "graph instantiate");
-            cudaGraphDestroy(g);
-        }
+        if (cfg.use_graph) pipe.graph = capture_graph(s, [&] { enqueue_iteration(0, 0.0, true); });
         pipe.ready = true;
     }
     if (m > pipe.cap) {
@@ -2103,9 +2108,11 @@ int Solver::stage_lusgs(const double* U, const double* R, const double* dU_prev,
     D.dt_out = d_dt;
     D.S_out = d_S;
     for (int c = 0; c < I.C; ++c)
-        k_forward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c, cfl);
+        if (Q.oe[c] > Q.gs[c])
+            k_forward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c, cfl);
     for (int c = I.C - 2; c >= 0; --c)
-        k_backward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c);
+        if (Q.oe[c] > Q.gs[c])
+            k_backward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c);
     ck(cudaGetLastError(), "lusgs launch");
     auto grab1 = [&](double* h, const double* d) {
         if (!h) return;
@@ -2204,7 +2211,7 @@ void probe(int mode, int n, const double* U, const double* dU, int axis, int sig
     ck(cudaMalloc(&dst, sizeof(int) * std::max(n, 1)), "cudaMalloc");
     ck(cudaMemcpy(dU_, U, sizeof(double4) * n, cudaMemcpyHostToDevice), "H2D");
     if (dU) ck(cudaMemcpy(ddU, dU, sizeof(double4) * n, cudaMemcpyHostToDevice), "H2D");
-    k_probe<<<blocks_for(n, 128), 128>>>(n, mode, dU_, ddU, axis, sign, exact, dout, dst);
+    if (n > 0) k_probe<<<blocks_for(n, 128), 128>>>(n, mode, dU_, ddU, axis, sign, exact, dout, dst);
     ck(cudaGetLastError(), "probe launch");
     ck(cudaMemcpy(out, dout, sizeof(double4) * n, cudaMemcpyDeviceToHost), "D2H");
     if (status) ck(cudaMemcpy(status, dst, sizeof(int) * n, cudaMemcpyDeviceToHost), "D2H");
@@ -2226,7 +2233,7 @@ void probe_math(int n, int which, const double* x, double* lib, double* mine)
     ck(cudaMalloc(&dl, b), "cudaMalloc");
     ck(cudaMalloc(&dm, b), "cudaMalloc");
     ck(cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
-    k_mathprobe<<<blocks_for(n, 256), 256>>>(n, which, dx, dl, dm);
+    if (n > 0) k_mathprobe<<<blocks_for(n, 256), 256>>>(n, which, dx, dl, dm);
     ck(cudaGetLastError(), "mathprobe launch");
     ck(cudaMemcpy(lib, dl, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(mine, dm, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");

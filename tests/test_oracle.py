@@ -195,3 +195,26 @@ def test_oracle_vs_live_reference_lattice_and_freestream():
     Ra, _ = ref.residual(q, gx, gy, first_order=True)
     Rb, _ = o.residual(q, gx, gy, first_order=True)
     assert np.array_equal(Ra, Rb)
+
+
+def _matrix():
+    m = np.load(os.path.join(os.path.dirname(__file__), "golden", "config_matrix.npz"))
+    return m, json.loads(str(m["meta"]))
+
+
+@pytest.mark.parametrize("name", sorted(_matrix()[1]))
+def test_oracle_config_matrix_bitwise(name):
+    """The restatement over the configuration matrix (n_inner 1/2/4, CFL ramp,
+    free-stream BCs, cambered section, convergence/divergence stops, pressure,
+    explicit and first-iteration aborts): bitwise the reference fixtures."""
+    m, meta = _matrix()
+    case = meta[name]
+    c = kf.generate_naca_ogrid(*case["cloud"])
+    nb = c.nbr
+    o = Oracle(c.x, c.y, c.kind, c.normal_x, c.normal_y, nb.offsets, nb.ids)
+    r = o.run(**case["cfg"])
+    assert len(r.residual) == case["iters"] and r.abort_reason == case["reason"]
+    assert np.array_equal(r.residual, m[name + "_residual"])
+    assert np.array_equal(r.cl, m[name + "_cl"]) and np.array_equal(r.cd, m[name + "_cd"])
+    assert np.array_equal(r.first_order, m[name + "_first_order"])
+    assert np.array_equal(r.final_state, m[name + "_final"])
