@@ -218,3 +218,18 @@ def test_oracle_config_matrix_bitwise(name):
     assert np.array_equal(r.cl, m[name + "_cl"]) and np.array_equal(r.cd, m[name + "_cd"])
     assert np.array_equal(r.first_order, m[name + "_first_order"])
     assert np.array_equal(r.final_state, m[name + "_final"])
+
+
+@pytest.mark.parametrize("variant", ["explicit", "anandh", "anandh_ad", "manish", "manish_ad"])
+def test_oracle_irregular_cloud_bitwise(golden, variant):
+    """Jittered O-grid with random extra neighbours (degrees 5..19, 10
+    colours; tests/golden/make_irregular.py), incl. the incremental
+    sweep's invalid-increment abort: the restatement is bitwise the
+    reference."""
+    g = np.load(os.path.join(golden, "irregular_histories.npz"))
+    o = Oracle(g["x"], g["y"], g["kind"], g["nx"], g["ny"], g["off"], g["ids"])
+    r = o.run(variant=variant, n_iterations=40, mach=0.63, aoa_deg=2.0, cfl=0.05 if variant == "explicit" else 0.2)
+    assert r.abort_reason == str(g[variant + "_reason"])
+    assert np.array_equal(r.residual, g[variant + "_residual"])
+    assert np.array_equal(r.cl, g[variant + "_cl"]) and np.array_equal(r.cd, g[variant + "_cd"])
+    assert np.array_equal(r.final_state, g[variant + "_final"])
