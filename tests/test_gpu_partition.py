@@ -137,3 +137,16 @@ def test_nccl_transport_single_rank(small):
     ref = kf.Solver(small, cfg("manish_ad", n_iterations=40))
     want, rec1 = ref.step_host(U, dU)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_many_partitions_and_eager_launches(small, use_graph):
+    """12 Morton partitions of a 576-point cloud (partitions with empty colour
+    blocks, many peers) and the eager (non-graph) launch path: states bitwise
+    the unpartitioned graph run."""
+    one = kf.Solver(small, cfg("anandh", n_iterations=25)).run()
+    r = kf.Solver(small, cfg("anandh", n_iterations=25, use_graph=use_graph), n_parts=12,
+                  partition="morton").run()
+    assert len(r.iters) == len(one.iters) and r.abort_reason == one.abort_reason
+    assert np.array_equal(r.final_state, one.final_state)
+    assert relmax(r.residual, one.residual) <= 1e-13 and np.array_equal(r.cl, one.cl)
