@@ -280,14 +280,32 @@ struct Solver::Impl {
     // neighbour gathers of the gradient / residual kernels: 1 SMEM-staged
     // tiles (default), 0 global-gather sliced ELL (A/B reference)
     int gather = 1;
+    int pdl = 1;  // programmatic dependent launch of the iteration kernels (KF_PDL=0: off)
+    // launch on the context stream, with programmatic stream serialisation
+    // when enabled (the kernel's prologue overlaps its predecessor's drain)
+    template <class... KArgs, class... Args>
+    void launch(void (*k)(KArgs...), int grid, int block, size_t smem, Args... args)
+    {
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(block);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = pdl ? 1 : 0;
+        ck(cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...), "launch");
+    }
     int fused_tail = 0;  // KF_FUSED_TAIL=1: k_update_fin (update + finalize in one launch)
     void launch_grad(Part& P, bool first, int src, int dst)
     {
         if (gather) {
             if (first)
-                k_grad_t<true><<<P.n_tiles, kTile, P.tile_smem1, s>>>(P.D, src, dst);
+                launch(k_grad_t<true>, P.n_tiles, kTile, P.tile_smem1, P.D, src, dst);
             else
-                k_grad_t<false><<<P.n_tiles, kTile, P.tile_smem, s>>>(P.D, src, dst);
+                launch(k_grad_t<false>, P.n_tiles, kTile, P.tile_smem, P.D, src, dst);
             return;
         }
         if (first)
@@ -300,11 +318,11 @@ struct Solver::Impl {
         if (gather) {
             const size_t sm = P.tile_smem;
             switch (flux_variant) {
-                case 1: k_residual_t<4, false><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
-                case 2: k_residual_t<3, true><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
-                case 3: k_residual_t<4, true><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
-                case 4: k_residual_t<5, true><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
-                default: k_residual_t<3, false><<<P.n_tiles, kTile, sm, s>>>(P.D, gslot, 0); break;
+                case 1: launch(k_residual_t<4, false>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
+                case 2: launch(k_residual_t<3, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
+                case 3: launch(k_residual_t<4, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
+                case 4: launch(k_residual_t<5, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
+                default: launch(k_residual_t<3, false>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
             }
             return;
         }
@@ -372,6 +390,8 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // A/B switch for the neighbour gathers of the gradient/residual kernels
         const char* g = std::getenv("KF_GATHER");
         gather = (g && std::string(g) == "ell") ? 0 : 1;
+        const char* pe = std::getenv("KF_PDL");
+        pdl = !(pe && std::string(pe) == "0");
         const char* ft = std::getenv("KF_FUSED_TAIL");
         fused_tail = ft && std::string(ft) == "1";
     }
@@ -1469,7 +1489,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
         for (int c = 0; c < C; ++c) {
             for (Part& P : parts) {
                 if (P.oe[c] == P.gs[c]) continue;  // no owned point of this colour here
-                k_forward<<<blocks_for(P.oe[c] - P.gs[c], T), T, 0, s>>>(P.D, cb, c, cfl_override);
+                launch(k_forward, blocks_for(P.oe[c] - P.gs[c], T), T, 0, P.D, cb, c, cfl_override);
                 mark("lusgs_forward");
             }
             if (halo && C > 1) exchange_j(c);
@@ -1477,7 +1497,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
         for (int c = C - 2; c >= 0; --c) {
             for (Part& P : parts) {
                 if (P.oe[c] == P.gs[c]) continue;
-                k_backward<<<blocks_for(P.oe[c] - P.gs[c], T), T, 0, s>>>(P.D, cb, c);
+                launch(k_backward, blocks_for(P.oe[c] - P.gs[c], T), T, 0, P.D, cb, c);
                 mark("lusgs_backward");
             }
             if (halo && c > 0) exchange_j(c);
@@ -1489,7 +1509,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
         return;
     }
     for (Part& P : parts) {
-        k_update<<<blocks_for(P.n_pad, 256), 256, 0, s>>>(P.D, cb, cfl_override);
+        launch(k_update, blocks_for(P.n_pad, 256), 256, 0, P.D, cb, cfl_override);
         mark("update_bc_q");
     }
     if (halo) {
@@ -1503,7 +1523,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
             mark("finalize");
         }
     } else {
-        k_finalize<false><<<1, 1024, 0, s>>>(parts[0].D);
+        launch(k_finalize<false>, 1, 1024, 0, parts[0].D);
         mark("finalize");
     }
 }
