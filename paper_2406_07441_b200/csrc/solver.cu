@@ -298,7 +298,6 @@ struct Solver::Impl {
         lc.numAttrs = pdl ? 1 : 0;
         ck(cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...), "launch");
     }
-    int fused_tail = 0;  // KF_FUSED_TAIL=1: k_update_fin (update + finalize in one launch)
     void launch_grad(Part& P, bool first, int src, int dst)
     {
         if (gather) {
@@ -392,8 +391,6 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         gather = (g && std::string(g) == "ell") ? 0 : 1;
         const char* pe = std::getenv("KF_PDL");
         pdl = !(pe && std::string(pe) == "0");
-        const char* ft = std::getenv("KF_FUSED_TAIL");
-        fused_tail = ft && std::string(ft) == "1";
     }
     std::vector<double> oty, otx;
     setup_globals(c, oty, otx);
@@ -1254,11 +1251,6 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     ck(cudaMemsetAsync(D.fb_part, 0, sizeof(int), s), "memset");
     D.n_res_blocks = gather ? P.n_tiles : P.n_tile_blocks;  // blocks of the residual launch
     D.status = dalloc<unsigned long long>(1, owned);
-    {
-        unsigned* t = dalloc<unsigned>(1, owned);
-        ck(cudaMemsetAsync(t, 0, sizeof(unsigned), s), "memset");
-        D.ticket = t;
-    }
     D.iter = dalloc<int>(1, owned);
     D.nrec = dalloc<int>(1, owned);
     D.res0 = dalloc<double>(1, owned);
@@ -1502,11 +1494,6 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
             }
             if (halo && c > 0) exchange_j(c);
         }
-    }
-    if (!halo && fused_tail) {
-        k_update_fin<<<blocks_for(parts[0].n_pad, 256), 256, 0, s>>>(parts[0].D, cb, cfl_override);
-        mark("update_bc_q_finalize");
-        return;
     }
     for (Part& P : parts) {
         launch(k_update, blocks_for(P.n_pad, 256), 256, 0, P.D, cb, cfl_override);
