@@ -576,7 +576,7 @@ kf_status kf_stage_forces(kf_ctx* ctx, const double* U, double* cl, double* cd)
 kf_status kf_probe_math(int n, int which, const double* x, double* lib, double* mine)
 {
     return guarded([&] {
-        if (which < 0 || which > 2) return err(KF_CONFIG, "which must be 0 (exp), 1 (log) or 2 (erf)");
+        if (which < 0 || which > 3) return err(KF_CONFIG, "which must be 0 (exp), 1 (log), 2 (erf) or 3 (division)");
         kfb::probe_math(n, which, x, lib, mine);
         return ok();
     });

@@ -321,6 +321,8 @@ struct Solver::Impl {
                 case 2: launch(k_residual_t<3, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
                 case 3: launch(k_residual_t<4, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
                 case 4: launch(k_residual_t<5, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
+                case 5: launch(k_residual_t<4, true, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
+                case 6: launch(k_residual_t<3, true, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
                 default: launch(k_residual_t<3, false>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
             }
             return;
@@ -385,7 +387,7 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // A/B switch for the residual kernel (register cap x arithmetic)
         const char* env = std::getenv("KF_FLUX_KERNEL");
         const std::string v = env ? env : "m4fast";
-        flux_variant = v == "m3" ? 0 : v == "m4" ? 1 : v == "m3fast" ? 2 : v == "m5fast" ? 4 : 3;
+        flux_variant = v == "m3" ? 0 : v == "m4" ? 1 : v == "m3fast" ? 2 : v == "m5fast" ? 4 : v == "m4pair" ? 5 : v == "m3pair" ? 6 : 3;
         // A/B switch for the neighbour gathers of the gradient/residual kernels
         const char* g = std::getenv("KF_GATHER");
         gather = (g && std::string(g) == "ell") ? 0 : 1;
@@ -1215,6 +1217,8 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         ck(cudaFuncSetAttribute(k_residual_t<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<5, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t<4, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t<3, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
     }
 
     for (int b = 0; b < 2; ++b) {
@@ -2236,10 +2240,11 @@ void probe_math(int n, int which, const double* x, double* lib, double* mine)
         throw SolverError(KF_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
     double *dx = nullptr, *dl = nullptr, *dm = nullptr;
     const size_t b = sizeof(double) * std::max(n, 1);
-    ck(cudaMalloc(&dx, b), "cudaMalloc");
     ck(cudaMalloc(&dl, b), "cudaMalloc");
     ck(cudaMalloc(&dm, b), "cudaMalloc");
-    ck(cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+    const size_t nx = which == 3 ? 2 * (size_t)n : (size_t)n;  // division: (a, b) pairs
+    ck(cudaMalloc(&dx, sizeof(double) * std::max<size_t>(nx, 1)), "cudaMalloc");
+    ck(cudaMemcpy(dx, x, sizeof(double) * nx, cudaMemcpyHostToDevice), "H2D");
     if (n > 0) k_mathprobe<<<blocks_for(n, 256), 256>>>(n, which, dx, dl, dm);
     ck(cudaGetLastError(), "mathprobe launch");
     ck(cudaMemcpy(lib, dl, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
