@@ -1041,7 +1041,8 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         }
         thalo.resize(thoff.back());
         tell.resize(teoff.back());
-        tw.resize(twoff.back());
+        // + 2 rows of padding: the residual preloads two weights per entry
+        tw.resize(twoff.back() + 2 * kTile, 0.0);
         tpts.assign(static_cast<size_t>(n_tiles) * kTile, -1);
         tlsf.assign(tpts.size(), make_double4(0, 0, 0, 0));
         tlsfd.assign(tpts.size(), make_double2(1, 1));
