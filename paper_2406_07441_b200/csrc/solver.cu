@@ -816,7 +816,9 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     // when a region runs out, each tile <= kTile points and <= kHaloCap
     // staged records; KF_TILE_ORDER=morton = plain Morton chunks. Content
     // (parallel over tiles): slots, 16-bit entries, weight stream.
-    std::vector<int> tpts, thoff(1, 0), thalo, teoff(1, 0);
+    std::vector<int> tpts, thalo;
+    std::vector<int2> tmeta;
+    int h_stride = 8, e_stride = kTile;
     std::vector<unsigned short> tell;
     std::vector<double> tw;                  // streamed split weights (residual)
     std::vector<long long> twoff(1, 0);
@@ -1033,14 +1035,17 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         if (!tile_error.empty()) throw SolverError(KF_CONFIG, tile_error);
         // -- concatenate
         for (int ti = 0; ti < n_tiles; ++ti) {
-            thoff.push_back(thoff.back() + outs[ti].ns);
-            teoff.push_back(teoff.back() + static_cast<int>(outs[ti].ent.size()));
             twoff.push_back(twoff.back() + static_cast<long long>(outs[ti].w.size()));
             nh_max = std::max(nh_max, outs[ti].ns);
             P.w_max = std::max(P.w_max, outs[ti].W);
         }
-        thalo.resize(thoff.back());
-        tell.resize(teoff.back());
+        // fixed per-tile strides (see Dev::t_meta); + kTile ids of padding:
+        // the first staging batch loads 128 ids unconditionally
+        h_stride = std::max((nh_max + 7) & ~7, 8);
+        e_stride = std::max(P.w_max, 1) * kTile;
+        thalo.assign(static_cast<size_t>(n_tiles) * h_stride + kTile, 0);
+        tell.assign(static_cast<size_t>(n_tiles) * e_stride, 0);
+        tmeta.resize(n_tiles);
         // + 2 rows of padding: the residual preloads two weights per entry
         tw.resize(twoff.back() + 2 * kTile, 0.0);
         tpts.assign(static_cast<size_t>(n_tiles) * kTile, -1);
@@ -1051,8 +1056,9 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         tlsD.assign(tpts.size(), make_double4(1, 1, 1, 1));
 #pragma omp parallel for schedule(static)
         for (int ti = 0; ti < n_tiles; ++ti) {
-            std::copy(outs[ti].halo.begin(), outs[ti].halo.end(), thalo.begin() + thoff[ti]);
-            std::copy(outs[ti].ent.begin(), outs[ti].ent.end(), tell.begin() + teoff[ti]);
+            std::copy(outs[ti].halo.begin(), outs[ti].halo.end(), thalo.begin() + static_cast<size_t>(ti) * h_stride);
+            std::copy(outs[ti].ent.begin(), outs[ti].ent.end(), tell.begin() + static_cast<size_t>(ti) * e_stride);
+            tmeta[ti] = make_int2(outs[ti].ns, outs[ti].W);
             std::copy(outs[ti].w.begin(), outs[ti].w.end(), tw.begin() + twoff[ti]);
             const int m = tile_off[ti + 1] - tile_off[ti];
             for (int t = 0; t < m; ++t) {
@@ -1074,10 +1080,11 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             tlsA.assign(kTile, make_double4(0, 0, 0, 0));
             tlsB = tlsA;
             tlsD.assign(kTile, make_double4(1, 1, 1, 1));
-            thoff.push_back(0);
-            teoff.push_back(0);
-            thalo.push_back(0);
-            tell.push_back(0);
+            h_stride = 8;
+            e_stride = kTile;
+            thalo.assign(h_stride + kTile, 0);
+            tell.assign(e_stride, 0);
+            tmeta.assign(1, make_int2(0, 0));
             twoff.push_back(0);
             tw.push_back(0.0);
             P.n_tiles = 1;
@@ -1187,9 +1194,12 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         D.nh_cap = P.nh_cap;
         D.w_max = P.w_max;
         D.t_pts = upi(tpts);
-        D.t_hoff = upi(thoff);
+        D.h_stride = h_stride;
+        D.e_stride = e_stride;
+        int2* d_meta = dalloc<int2>(tmeta.size(), owned);
+        up(d_meta, tmeta);
+        D.t_meta = d_meta;
         D.t_halo = upi(thalo);
-        D.t_eoff = upi(teoff);
         unsigned short* d_ell = dalloc<unsigned short>(tell.size(), owned);
         up(d_ell, tell);
         D.t_ell = d_ell;
@@ -1204,7 +1214,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         long long* d_twoff = dalloc<long long>(twoff.size(), owned);
         up(d_twoff, twoff);
         D.t_woff = d_twoff;
-        const size_t ent_bytes = static_cast<size_t>(P.w_max) * kTile * sizeof(unsigned short);
+        const size_t ent_bytes = static_cast<size_t>(e_stride) * sizeof(unsigned short);
         P.tile_smem = static_cast<size_t>(kTileUnits) * P.nh_cap * sizeof(double2) + ent_bytes;
         P.tile_smem1 = static_cast<size_t>(3) * P.nh_cap * sizeof(double2) + ent_bytes;
         if (P.tile_smem > kMaxTileSmem) throw SolverError(KF_CONFIG, "tile staging exceeds shared memory");
