@@ -1039,11 +1039,11 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             nh_max = std::max(nh_max, outs[ti].ns);
             P.w_max = std::max(P.w_max, outs[ti].W);
         }
-        // fixed per-tile strides (see Dev::t_meta); + kTile ids of padding:
-        // the first staging batch loads 128 ids unconditionally
+        // fixed per-tile strides (see Dev::t_meta); + 4 kTile ids of padding:
+        // a staging batch loads up to 512 ids unconditionally
         h_stride = std::max((nh_max + 7) & ~7, 8);
         e_stride = std::max(P.w_max, 1) * kTile;
-        thalo.assign(static_cast<size_t>(n_tiles) * h_stride + kTile, 0);
+        thalo.assign(static_cast<size_t>(n_tiles) * h_stride + 4 * kTile, 0);
         tell.assign(static_cast<size_t>(n_tiles) * e_stride, 0);
         tmeta.resize(n_tiles);
         // + 2 rows of padding: the residual preloads two weights per entry
@@ -1082,7 +1082,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             tlsD.assign(kTile, make_double4(1, 1, 1, 1));
             h_stride = 8;
             e_stride = kTile;
-            thalo.assign(h_stride + kTile, 0);
+            thalo.assign(h_stride + 4 * kTile, 0);
             tell.assign(e_stride, 0);
             tmeta.assign(1, make_int2(0, 0));
             twoff.push_back(0);
