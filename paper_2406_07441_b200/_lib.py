@@ -31,7 +31,7 @@ EXPORTED = [
     "kf_device_count", "kf_profile_kernels", "kf_measure_fp64_peak",
     "kf_partition_plan", "kf_layout_build", "kf_layout_free", "kf_layout_sizes",
     "kf_layout_arrays", "kf_layout_send", "kf_layout_recv", "kf_create_partitioned",
-    "kf_nccl_unique_id", "kf_create_rank", "kf_n_parts", "kf_owned_points", "kf_step_host_batch",
+    "kf_nccl_unique_id", "kf_create_rank", "kf_create_rank_host", "kf_n_parts", "kf_owned_points", "kf_step_host_batch",
     "kf_probe_math",
 ]
 
@@ -68,6 +68,10 @@ _ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 _vp = C.c_void_p
 _S = Status
 _pp = C.POINTER(C.c_void_p)
+# kf_exchange_fn / kf_allreduce_fn (include/kf.h, host-staged transport)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                          C.POINTER(C.c_void_p), C.POINTER(C.c_size_t))
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_size_t)
 
 
 def _load():
@@ -130,6 +134,8 @@ def _load():
         "kf_create_partitioned": (_S, [_vp, C.POINTER(Config), C.c_int, C.c_int, _pp]),
         "kf_nccl_unique_id": (_S, [C.c_char_p]),
         "kf_create_rank": (_S, [_vp, C.POINTER(Config), C.c_int, C.c_int, C.c_int, C.c_char_p, _pp]),
+        "kf_create_rank_host": (_S, [_vp, C.POINTER(Config), C.c_int, C.c_int, C.c_int, EXCHANGE_FN,
+                                     ALLREDUCE_FN, _vp, _pp]),
         "kf_n_parts": (C.c_int, [_vp]),
         "kf_owned_points": (C.c_int, [_vp]),
         "kf_version": (C.c_char_p, []),

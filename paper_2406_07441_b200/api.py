@@ -398,6 +398,37 @@ def _records(buf, n):
 _PART_MODES = {"angular": L.KF_PART_ANGULAR, "morton": L.KF_PART_MORTON}
 
 
+def _host_callbacks(exchange, allreduce):
+    """ctypes trampolines for kf_exchange_fn / kf_allreduce_fn (a Python
+    exception becomes a nonzero return: the library raises KF_RUNTIME)."""
+    from . import _lib
+
+    def exch(_user, n, peer, is_send, buf, nbytes):
+        try:
+            msgs = []
+            for k in range(n):
+                b = int(nbytes[k])
+                arr = np.ctypeslib.as_array(C.cast(buf[k], C.POINTER(C.c_uint8)), shape=(b,))
+                msgs.append((int(peer[k]), bool(is_send[k]), arr))
+            exchange(msgs)
+            return 0
+        except Exception:  # pragma: no cover - reported as KF_RUNTIME
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def ared(_user, buf, n):
+        try:
+            allreduce(np.ctypeslib.as_array(buf, shape=(int(n),)))
+            return 0
+        except Exception:  # pragma: no cover
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    return _lib.EXCHANGE_FN(exch), _lib.ALLREDUCE_FN(ared)
+
+
 def _part_mode(mode) -> int:
     if isinstance(mode, str):
         if mode not in _PART_MODES:
@@ -422,7 +453,13 @@ class Solver:
         self.n = cloud.n()
         self._cfg = config.to_c()
         h = C.c_void_p()
-        if _rank is not None:
+        self._callbacks = None
+        if _rank is not None and len(_rank) == 4:
+            n_ranks, rank, exchange, allreduce = _rank
+            self._callbacks = _host_callbacks(exchange, allreduce)  # kept alive with the context
+            _check(lib.kf_create_rank_host(cloud.handle, C.byref(self._cfg), n_ranks, rank, _part_mode(partition),
+                                           self._callbacks[0], self._callbacks[1], None, C.byref(h)))
+        elif _rank is not None:
             n_ranks, rank, nccl_id = _rank
             _check(lib.kf_create_rank(cloud.handle, C.byref(self._cfg), n_ranks, rank, _part_mode(partition),
                                       nccl_id, C.byref(h)))
@@ -442,6 +479,18 @@ class Solver:
         arrays keep the whole-cloud shape; only this rank's owned entries are
         written."""
         return cls(cloud, config, partition=partition, _rank=(n_ranks, rank, nccl_id))
+
+    @classmethod
+    def for_rank_host(cls, cloud: PointCloud, config: SolverConfig, n_ranks: int, rank: int, exchange,
+                      allreduce, partition="angular") -> "Solver":
+        """Partition `rank` of an `n_ranks`-way decomposition over any host
+        communicator (kf_create_rank_host): ``exchange(msgs)`` receives the
+        step's posted messages as a list of ``(peer, is_send, buffer)`` with
+        `buffer` a writable uint8 numpy view of pinned host memory, in
+        posting order (the k-th send to a peer matches that peer's k-th
+        receive), and must move them; ``allreduce(buf)`` sums a float64
+        numpy array in place across the ranks. Launches are eager."""
+        return cls(cloud, config, partition=partition, _rank=(n_ranks, rank, exchange, allreduce))
 
     @property
     def n_parts(self) -> int:

@@ -339,6 +339,28 @@ kf_status kf_create_rank(const kf_cloud* cloud, const kf_config* cfg, int n_rank
     return create_ctx(cloud, cfg, spec, out);
 }
 
+kf_status kf_create_rank_host(const kf_cloud* cloud, const kf_config* cfg, int n_ranks, int rank, int mode,
+                              kf_exchange_fn exch, kf_allreduce_fn allreduce, void* user, kf_ctx** out)
+{
+    if (!exch || !allreduce) {
+        *out = nullptr;
+        return err(KF_CONFIG, "kf_create_rank_host: missing exchange or allreduce callback");
+    }
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) {
+        *out = nullptr;
+        return err(KF_CONFIG, "rank out of range");
+    }
+    kfb::PartitionSpec spec;
+    spec.n_parts = n_ranks;
+    spec.mode = mode;
+    spec.rank = rank;
+    spec.host = 1;
+    spec.exch = exch;
+    spec.allreduce = allreduce;
+    spec.user = user;
+    return create_ctx(cloud, cfg, spec, out);
+}
+
 int kf_n_parts(const kf_ctx* ctx) { return ctx->solver->n_parts(); }
 int kf_owned_points(const kf_ctx* ctx) { return ctx->solver->owned_points(); }
 

@@ -169,7 +169,7 @@ cudaGraphExec_t capture_graph(cudaStream_t st, F&& enqueue)
     return x;
 }
 
-enum Transport : int { kSingle = 0, kInProc = 1, kNccl = 2 };
+enum Transport : int { kSingle = 0, kInProc = 1, kNccl = 2, kHost = 3 };
 
 // staged records per tile (own points + stencil neighbours); 767 x 14 doubles
 // = 86 KB of shared memory at most (NACA O-grids need <= 372)
@@ -270,6 +270,16 @@ struct Solver::Impl {
     Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spec);
     ~Impl();
     bool multi() const { return transport != kSingle; }
+    // one partition of a multi-process run (this rank's points only cross PCIe)
+    bool per_rank() const { return transport == kNccl || transport == kHost; }
+    // host-staged transport: the caller's communicator and a pinned staging area
+    kf_exchange_fn h_exch = nullptr;
+    kf_allreduce_fn h_allreduce = nullptr;
+    void* h_user = nullptr;
+    char* h_stage = nullptr;
+    size_t h_stage_bytes = 0;
+    double* h_red = nullptr;
+    void host_exchange();
     Part& p0() { return parts[0]; }
     void pack(const Cloud& c, const LocalLayout& L, const std::vector<uint64_t>& code,
               const std::vector<double>& oty, const std::vector<double>& otx, double* red_shared,
@@ -380,8 +390,15 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
     C = std::max(c.n_colors, 1);
     if (spec.n_parts < 1) throw SolverError(KF_CONFIG, "n_parts must be >= 1");
     n_rows = spec.n_parts;
-    transport = spec.nccl ? kNccl : (spec.n_parts == 1 ? kSingle : kInProc);
-    if (transport == kNccl && (spec.rank < 0 || spec.rank >= spec.n_parts))
+    transport = spec.host ? kHost : spec.nccl ? kNccl : (spec.n_parts == 1 ? kSingle : kInProc);
+    if (transport == kHost) {
+        if (!spec.exch || !spec.allreduce) throw SolverError(KF_CONFIG, "host transport needs exchange and allreduce");
+        h_exch = spec.exch;
+        h_allreduce = spec.allreduce;
+        h_user = spec.user;
+        cfg.use_graph = 0;  // host work between the stages
+    }
+    if (per_rank() && (spec.rank < 0 || spec.rank >= spec.n_parts))
         throw SolverError(KF_CONFIG, "rank out of range");
     {
         // A/B switch for the residual kernel (register cap x arithmetic)
@@ -410,7 +427,7 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         ck(cudaMemsetAsync(red_shared, 0, sizeof(double) * red_len, s), "memset");
     }
     std::vector<int> ranks;
-    if (transport == kNccl)
+    if (per_rank())
         ranks.push_back(spec.rank);
     else
         for (int r = 0; r < n_rows; ++r) ranks.push_back(r);
@@ -461,6 +478,8 @@ Solver::Impl::~Impl()
         if (g) cudaGraphExecDestroy(g);
     if (bench_graph) cudaGraphExecDestroy(bench_graph);
     if (comm) nccl().CommDestroy(comm);
+    if (h_stage) cudaFreeHost(h_stage);
+    if (h_red) cudaFreeHost(h_red);
     for (void* p : owned) cudaFree(p);
     for (auto& P : parts)
         if (P.hcomp) cudaFreeHost(P.hcomp);
@@ -1326,7 +1345,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         P.sendB = dalloc<unsigned char>(P.n_send, owned);
     }
     // compact transfers (multi-process)
-    if (transport == kNccl) {
+    if (per_rank()) {
         int* d_own = dalloc<int>(own_loc.size(), owned);
         up(d_own, own_loc);
         P.d_own = d_own;
@@ -1377,6 +1396,46 @@ void Solver::Impl::post(Part& P, bool send, int peer, void* buf, size_t bytes)
     msgs.push_back(Msg{P.rank, peer, send, buf, bytes});
 }
 
+// Host-staged exchange: the posted sends go device -> pinned host, the
+// caller's communicator moves the whole list (posting order), the receives go
+// host -> device. The stream is synchronised first (the packed send buffers)
+// and the receive copies are stream-ordered before the next stage.
+void Solver::Impl::host_exchange()
+{
+    ck(cudaStreamSynchronize(s), "host exchange: sync");
+    size_t total = 0;
+    for (const Msg& m : msgs) total += (m.bytes + 15) & ~size_t(15);
+    if (total > h_stage_bytes) {
+        if (h_stage) cudaFreeHost(h_stage);
+        h_stage = nullptr;
+        ck(cudaMallocHost(reinterpret_cast<void**>(&h_stage), std::max<size_t>(total, 16)), "cudaMallocHost");
+        h_stage_bytes = std::max<size_t>(total, 16);
+    }
+    const int nm = static_cast<int>(msgs.size());
+    std::vector<int> peer(nm), is_send(nm);
+    std::vector<void*> hb(nm);
+    std::vector<size_t> nb(nm);
+    size_t off = 0;
+    for (int k = 0; k < nm; ++k) {
+        const Msg& m = msgs[k];
+        peer[k] = m.peer;
+        is_send[k] = m.send ? 1 : 0;
+        hb[k] = h_stage + off;
+        nb[k] = m.bytes;
+        if (m.send) ck(cudaMemcpyAsync(hb[k], m.buf, m.bytes, cudaMemcpyDeviceToHost, s), "host exchange: D2H");
+        off += (m.bytes + 15) & ~size_t(15);
+    }
+    ck(cudaStreamSynchronize(s), "host exchange: D2H");
+    if (nm && h_exch(h_user, nm, peer.data(), is_send.data(), hb.data(), nb.data()) != 0)
+        throw SolverError(KF_RUNTIME, "host exchange: the communicator callback failed");
+    for (int k = 0; k < nm; ++k)
+        if (!msgs[k].send)
+            ck(cudaMemcpyAsync(msgs[k].buf, hb[k], msgs[k].bytes, cudaMemcpyHostToDevice, s), "host exchange: H2D");
+    // the staging area is reused by the next exchange only after its
+    // leading synchronisation, so the H2D copies need no wait here
+    msgs.clear();
+}
+
 void Solver::Impl::begin_exchange()
 {
     msgs.clear();
@@ -1387,6 +1446,10 @@ void Solver::Impl::flush_exchange()
 {
     if (transport == kNccl) {
         nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+        return;
+    }
+    if (transport == kHost) {
+        host_exchange();
         return;
     }
     std::vector<char> used(msgs.size(), 0);
@@ -1457,9 +1520,19 @@ void Solver::Impl::exchange_j(int c)
 // with the same buffer).
 void Solver::Impl::reduce_rows()
 {
-    if (transport != kNccl) return;  // in-process partitions share one buffer
+    if (!per_rank()) return;  // in-process partitions share one buffer
     Part& A = p0();
     const size_t len = static_cast<size_t>(W) + kRowStride * static_cast<size_t>(n_rows);
+    if (transport == kHost) {
+        if (!h_red) ck(cudaMallocHost(reinterpret_cast<void**>(&h_red), sizeof(double) * len), "cudaMallocHost");
+        ck(cudaMemcpyAsync(h_red, A.red_local, sizeof(double) * len, cudaMemcpyDeviceToHost, s), "allreduce: D2H");
+        ck(cudaStreamSynchronize(s), "allreduce: sync");
+        if (h_allreduce(h_user, h_red, len) != 0)
+            throw SolverError(KF_RUNTIME, "host allreduce: the communicator callback failed");
+        ck(cudaMemcpyAsync(A.red, h_red, sizeof(double) * len, cudaMemcpyHostToDevice, s), "allreduce: H2D");
+        ck(cudaStreamSynchronize(s), "allreduce: H2D");  // h_red is reused next iteration
+        return;
+    }
     nccl_check(nccl().AllReduce(A.red_local, A.red, len, ncclFloat64, ncclSum, comm, s), "ncclAllReduce");
 }
 
@@ -1538,7 +1611,7 @@ void Solver::Impl::build_graphs()
 
 void Solver::Impl::upload_state(const double* host, const std::function<double4*(Part&)>& sel)
 {
-    if (transport != kNccl) {
+    if (!per_rank()) {
         h2d(dstage, reinterpret_cast<const double4*>(host), n, s);
         for (Part& P : parts)
             k_to_dev<<<blocks_for(P.n_pad, 256), 256, 0, s>>>(sel(P), dstage, P.D.orig, P.n_pad);
@@ -1558,7 +1631,7 @@ void Solver::Impl::upload_state(const double* host, const std::function<double4*
 
 void Solver::Impl::download_state(double* host, const std::function<const double4*(Part&)>& sel)
 {
-    if (transport != kNccl) {
+    if (!per_rank()) {
         for (Part& P : parts)
             k_to_ref<<<blocks_for(P.n_pad, 256), 256, 0, s>>>(dstage, sel(P), P.D.orig, P.D.kind, P.n_pad);
         d2h(reinterpret_cast<double4*>(host), dstage, n, s);
@@ -1768,7 +1841,7 @@ void Solver::bench_mode(int mode)
         I.bench = 0;
         return;
     }
-    if (!I.cfg.use_graph) {  // count the launches of one bench step
+    if (!I.cfg.use_graph && I.transport != kHost) {  // count the launches of one bench step
         const int saved = I.launches;
         cudaGraphExec_t x = capture_graph(I.s, [&] { I.enqueue_iteration(0, 0.0, false); });
         cudaGraphExecDestroy(x);
