@@ -85,3 +85,19 @@ def test_create_rank_validates_arguments():
     assert st.code == _lib.KF_CONFIG and b"NCCL unique id" in st.reason
     st = _lib.lib.kf_create_rank(c.handle, C.byref(cfg), 2, 2, 0, b"x" * 128, C.byref(h))
     assert st.code == _lib.KF_CONFIG and b"rank out of range" in st.reason
+
+
+def test_create_rank_host_validates_arguments():
+    """kf_create_rank_host: missing callbacks and bad ranks are configuration
+    errors (checked before any device work, so this runs without a GPU)."""
+    import ctypes as C
+    from paper_2406_07441_b200 import _lib
+    c = kf.generate_naca_ogrid("0012", 32, 8, 10.0)
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.ManishAD).to_c()
+    h = C.c_void_p()
+    ex = _lib.EXCHANGE_FN(lambda *a: 0)
+    ar = _lib.ALLREDUCE_FN(lambda *a: 0)
+    st = _lib.lib.kf_create_rank_host(c.handle, C.byref(cfg), 2, 0, 0, _lib.EXCHANGE_FN(), ar, None, C.byref(h))
+    assert st.code == _lib.KF_CONFIG and b"callback" in st.reason
+    st = _lib.lib.kf_create_rank_host(c.handle, C.byref(cfg), 2, 5, 0, ex, ar, None, C.byref(h))
+    assert st.code == _lib.KF_CONFIG and b"rank out of range" in st.reason
