@@ -243,7 +243,7 @@ struct Solver::Impl {
     long long total_counters[5] = {0, 0, 0, 0, 0};
     int forces_err = 0;
     int W = 0;
-    int flux_variant = 0;  // residual kernel: 0 exact/3 blocks, 1 exact/4, 2 fast/3, 3 fast/4
+    bool flux_exact = false;  // residual kernel: libdevice-exact m3 (KF_FLUX_KERNEL=m3) or m4fast
     int launches = 0;
     int launches_bench = 0;
     std::vector<DevRecord> rec_h;
@@ -326,24 +326,16 @@ struct Solver::Impl {
     {
         if (gather) {
             const size_t sm = P.tile_smem;
-            switch (flux_variant) {
-                case 1: launch(k_residual_t<4, false>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
-                case 2: launch(k_residual_t<3, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
-                case 3: launch(k_residual_t<4, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
-                case 4: launch(k_residual_t<5, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
-                case 5: launch(k_residual_t<4, true, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
-                case 6: launch(k_residual_t<3, true, true>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
-                default: launch(k_residual_t<3, false>, P.n_tiles, kTile, sm, P.D, gslot, 0); break;
-            }
+            if (flux_exact)
+                launch(k_residual_t<3, false>, P.n_tiles, kTile, sm, P.D, gslot, 0);
+            else
+                launch(k_residual_t<4, true>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             return;
         }
-        switch (flux_variant) {
-            case 1: k_residual<4, false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
-            case 2: k_residual<3, true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
-            case 3:
-            case 4: k_residual<4, true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
-            default: k_residual<3, false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0); break;
-        }
+        if (flux_exact)
+            k_residual<3, false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0);
+        else
+            k_residual<4, true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, gslot, 0);
     }
     // halo exchanges and the cross-partition reduction
     struct Msg {
@@ -401,10 +393,11 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
     if (per_rank() && (spec.rank < 0 || spec.rank >= spec.n_parts))
         throw SolverError(KF_CONFIG, "rank out of range");
     {
-        // A/B switch for the residual kernel (register cap x arithmetic)
+        // A/B switch for the residual kernel: m4fast (default: division-free
+        // kinetics, 4 CTAs/SM) or m3 (libdevice-exact divisions and square
+        // roots, 3 CTAs/SM; the parity-margin reference)
         const char* env = std::getenv("KF_FLUX_KERNEL");
-        const std::string v = env ? env : "m4fast";
-        flux_variant = v == "m3" ? 0 : v == "m4" ? 1 : v == "m3fast" ? 2 : v == "m5fast" ? 4 : v == "m4pair" ? 5 : v == "m3pair" ? 6 : 3;
+        flux_exact = env && std::string(env) == "m3";
         // A/B switch for the neighbour gathers of the gradient/residual kernels
         const char* g = std::getenv("KF_GATHER");
         gather = (g && std::string(g) == "ell") ? 0 : 1;
@@ -1243,12 +1236,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         ck(cudaFuncSetAttribute(k_grad_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_grad_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_t<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_t<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_t<5, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_t<4, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_t<3, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
     }
 
     for (int b = 0; b < 2; ++b) {
