@@ -68,6 +68,8 @@ WARM_ITERS = 5
 # algorithmic bytes of the flux-residual kernel per point
 # (q 32 + qx,qy 64 + xy 16 + ids 4*n_s + R 32, n_s = split entries with w != 0)
 FLUX_BYTES_FIXED = 144.0
+# whole iteration, n_inner = 3, Manish: 144 + 2x176 + 144 + 176 + 121 + 121 + 97
+ITER_BYTES_FIXED = 1155.0
 
 
 def dist_env():
@@ -492,6 +494,29 @@ def main():
         except Exception:
             fp64 = None
 
+    # whole-iteration roofline: algorithmic bytes of all
+    # stages, the ncu FP64 count of all 13 launches, against the step time
+    n_f = float(len(cloud.nbr.ids)) / N
+    iter_bytes = n_own * (ITER_BYTES_FIXED + 4.0 * (3 * n_f + 3 * n_s))
+    step_s = ms_max / args.steps * 1e-3
+    iteration = {"alg_bytes": iter_bytes, "achieved_gbs": iter_bytes / step_s / 1e9,
+                 "hbm_frac": iter_bytes / step_s / 1e9 / hbm_peak,
+                 "how": "SURVEY.md 8(d) B_alg per point (144+4nf | 2x 176+4nf | 144+4ns | 176 | 2x 121+4ns | 97) "
+                        "x points / measured step time"}
+    ipath = os.path.join(ROOT, "profiles", "iter_fp64.json")
+    if os.path.exists(ipath) and world == 1 and args.parts == 1:
+        try:
+            with open(ipath) as f:
+                ij = json.load(f)
+            if ij.get("points") == N:
+                fl = float(ij["fp64_flops_per_iteration"])
+                t_ideal = max(iter_bytes / (hbm_peak * 1e9), fl / (fp64_peak * 1e12))
+                iteration.update({"fp64_flops": fl, "fp64_tflops": fl / step_s / 1e12,
+                                  "fp64_frac": fl / step_s / 1e12 / fp64_peak,
+                                  "t_ideal_over_t": t_ideal / step_s, "fp64_source": ij.get("source")})
+        except Exception:
+            pass
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -524,6 +549,7 @@ def main():
             "note": "the flux kernel is FP64-pipe bound (SURVEY.md F4); see fp64",
             "fp64_peak_tflops_measured": fp64_peak,
             "fp64": fp64,
+            "iteration": iteration,
         },
         "kernels_ms": {k: {"launches": v[0], "ms": v[1]} for k, v in agg.items()},
         "check": {"residual": recs[WARM_ITERS].residual if len(recs) > WARM_ITERS else None,

@@ -4,6 +4,7 @@
   python scripts/ncu_summary.py full   <report.ncu-rep> <out.json> [points]
   python scripts/ncu_summary.py launch <launches.csv>   <out.txt>
   python scripts/ncu_summary.py fp64   <fp64.csv>       <points>
+  python scripts/ncu_summary.py fp64_iter <fp64_iter.csv> <points>
 
 `full` keeps, per captured launch, duration, DRAM bytes, FP64-pipe and
 occupancy metrics; with `points` it also (re)writes profiles/flux_traffic.json
@@ -126,7 +127,38 @@ def fp64(path, points, out=None):
     print(tj)
 
 
+def fp64_iter(path, points, out=None):
+    """profiles/iter_fp64.json: FP64 flops (2 DFMA + DMUL + DADD) of every
+    kernel of one iteration (an ncu --csv --metrics capture of 13 launches)."""
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    hdr, data = rows[0], rows[1:]
+    ki, mi, vi, ids = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("ID")
+    per = collections.OrderedDict()
+    for r in data:
+        per.setdefault(r[ids], {"kernel": r[ki].split("(")[0]})[r[mi]] = float(r[vi].replace(",", ""))
+    kern = collections.OrderedDict()
+    total = 0.0
+    for l in per.values():
+        f = 2 * l.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", 0.0) + \
+            l.get("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0.0) + \
+            l.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0.0)
+        k = kern.setdefault(l["kernel"], {"launches": 0, "fp64_flops": 0.0})
+        k["launches"] += 1
+        k["fp64_flops"] += f
+        total += f
+    tj = {"points": int(points), "launches": len(per), "fp64_flops_per_iteration": total,
+          "fp64_flops_per_point": total / int(points), "kernels": kern, "source": os.path.basename(path),
+          "how": "ncu smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum of the 13 launches of "
+                 "one iteration; flops = 2 DFMA + DMUL + DADD"}
+    with open(out or os.path.join(ROOT, "profiles", "iter_fp64.json"), "w") as f:
+        json.dump(tj, f, indent=1)
+    print(json.dumps(tj, indent=1))
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "fp64_iter":
+        fp64_iter(sys.argv[2], sys.argv[3])
+        sys.exit(0)
     if sys.argv[1] == "fp64":
         fp64(sys.argv[2], sys.argv[3])
         sys.exit(0)
