@@ -243,7 +243,10 @@ struct Solver::Impl {
     long long total_counters[5] = {0, 0, 0, 0, 0};
     int forces_err = 0;
     int W = 0;
-    bool flux_exact = false;  // residual kernel: libdevice-exact m3 (KF_FLUX_KERNEL=m3) or m4fast
+    bool flux_exact = false;
+    // two threads per point in the flux kernel (clouds of < KF_RES_SPLIT_MAX
+    // points, default 200,000: a fraction of a wave of tiles, latency bound)
+    bool res_split = false;  // residual kernel: libdevice-exact m3 (KF_FLUX_KERNEL=m3) or m4fast
     int launches = 0;
     int launches_bench = 0;
     std::vector<DevRecord> rec_h;
@@ -328,6 +331,8 @@ struct Solver::Impl {
             const size_t sm = P.tile_smem;
             if (flux_exact)
                 launch(k_residual_t<3, false>, P.n_tiles, kTile, sm, P.D, gslot, 0);
+            else if (res_split)
+                launch(k_residual_t2<true>, P.n_tiles, 2 * kTile, sm, P.D, gslot, 0);
             else
                 launch(k_residual_t<4, true>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             return;
@@ -398,6 +403,8 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // roots, 3 CTAs/SM; the parity-margin reference)
         const char* env = std::getenv("KF_FLUX_KERNEL");
         flux_exact = env && std::string(env) == "m3";
+        const char* rs = std::getenv("KF_RES_SPLIT_MAX");
+        res_split = c.n < (rs ? std::atoi(rs) : 200000);
         // A/B switch for the neighbour gathers of the gradient/residual kernels
         const char* g = std::getenv("KF_GATHER");
         gather = (g && std::string(g) == "ell") ? 0 : 1;
@@ -1237,6 +1244,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         ck(cudaFuncSetAttribute(k_grad_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
     }
 
     for (int b = 0; b < 2; ++b) {

@@ -39,9 +39,28 @@ def test_tiling_does_not_change_states(env, which):
     else:
         g = np.load(os.path.join(os.path.dirname(__file__), "golden", "irregular_histories.npz"))
         c = kf.PointCloud.from_arrays(g["x"], g["y"], g["kind"], g["nx"], g["ny"], g["off"], g["ids"])
-    a = _run(c, {})
-    b = _run(c, env)
+    # (the global-gather path has one thread per point: compare it with the
+    # one-thread tile kernel, not the two-thread small-cloud variant)
+    base = {"KF_RES_SPLIT_MAX": "0"} if "KF_GATHER" in env else {}
+    a = _run(c, base)
+    b = _run(c, {**env, **base})
     assert len(a.iters) == len(b.iters) and a.abort_reason == b.abort_reason
     assert np.array_equal(a.final_state, b.final_state)
     assert np.array_equal(a.cl, b.cl) and np.array_equal(a.first_order, b.first_order)
     assert relmax(a.residual, b.residual) <= 1e-13
+
+
+@pytest.mark.parametrize("variant", ["manish_ad", "anandh"])
+def test_two_thread_flux_variant_matches_one_thread(variant):
+    """Clouds under KF_RES_SPLIT_MAX points run the flux kernel with two
+    threads per point (even / odd stencil entries, one extra addition): the
+    same demotions, tallies and abort record, states equal to rounding."""
+    c = kf.generate_naca_ogrid("0012", 160, 40, 15.0)
+    a = _run(c, {"KF_RES_SPLIT_MAX": "0"}, variant=kf.SolverVariant.parse(variant))
+    b = _run(c, {"KF_RES_SPLIT_MAX": "100000000"}, variant=kf.SolverVariant.parse(variant))
+    assert len(a.iters) == len(b.iters) and a.abort_reason == b.abort_reason
+    assert np.array_equal(a.first_order, b.first_order)
+    assert np.array_equal(np.array([i.counters for i in a.iters]), np.array([i.counters for i in b.iters]))
+    assert relmax(a.residual, b.residual) <= 1e-12
+    d = np.abs(a.final_state - b.final_state).max() / np.abs(a.final_state).max()
+    assert d <= 1e-12
