@@ -4,12 +4,19 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2406_07441_b200 as kf
 c = kf.generate_naca_ogrid("0012", 64, 16, 12.0)
-for variant in ("manish_ad", "anandh", "explicit"):
-    cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(variant), mach_inf=0.63, aoa_deg=2.0,
-                          cfl=0.05 if variant == "explicit" else 0.2, n_iterations=6)
-    for parts in (1, 3):
-        r = kf.Solver(c, cfg, n_parts=parts).run()
-        print(variant, parts, len(r.iters), r.abort_reason, flush=True)
+for env in ({}, {"KF_RES_SPLIT_MAX": "0"}, {"KF_FLUX_KERNEL": "m3"}):
+    # two-thread (small-cloud) and one-thread flux kernels, and the exact variant
+    for k in ("KF_RES_SPLIT_MAX", "KF_FLUX_KERNEL"):
+        os.environ.pop(k, None)
+    os.environ.update(env)
+    for variant in ("manish_ad", "anandh", "explicit"):
+        cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(variant), mach_inf=0.63, aoa_deg=2.0,
+                              cfl=0.05 if variant == "explicit" else 0.2, n_iterations=6)
+        for parts in (1, 3):
+            r = kf.Solver(c, cfg, n_parts=parts).run()
+            print(env, variant, parts, len(r.iters), r.abort_reason, flush=True)
+for k in ("KF_RES_SPLIT_MAX", "KF_FLUX_KERNEL"):
+    os.environ.pop(k, None)
 s = kf.Solver.for_rank(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD, n_iterations=4), 1, 0, kf.nccl_unique_id())
 print("nccl", len(s.run().iters))
 s = kf.Solver(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD, n_iterations=8))
