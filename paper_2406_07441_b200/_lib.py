@@ -19,7 +19,7 @@ KF_OK, KF_INVALID_STATE, KF_INVALID_INCREMENT, KF_DIVERGED, KF_CONFIG, KF_CUDA, 
 
 # every symbol include/kf.h declares (tests/test_abi.py checks the export list)
 EXPORTED = [
-    "kf_cloud_generate_naca", "kf_cloud_load", "kf_cloud_save", "kf_cloud_from_arrays",
+    "kf_cloud_generate_naca", "kf_cloud_load", "kf_cloud_save", "kf_cloud_save_binary", "kf_cloud_from_arrays",
     "kf_cloud_free", "kf_cloud_n", "kf_cloud_n_colors", "kf_cloud_set_colors",
     "kf_cloud_geometry", "kf_cloud_list_nnz", "kf_cloud_list", "kf_cloud_ls_full",
     "kf_cloud_ls_split", "kf_cloud_flagged", "kf_cloud_colors", "kf_cloud_report",
@@ -84,6 +84,7 @@ def _load():
         "kf_cloud_generate_naca": (_S, [C.c_char_p, C.c_int, C.c_int, C.c_double, _pp]),
         "kf_cloud_load": (_S, [C.c_char_p, _pp]),
         "kf_cloud_save": (_S, [_vp, C.c_char_p]),
+        "kf_cloud_save_binary": (_S, [_vp, C.c_char_p]),
         "kf_cloud_from_arrays": (_S, [C.c_int, _dp, _dp, _ip, _dp, _dp, _ip, _ip, _pp]),
         "kf_cloud_free": (None, [_vp]),
         "kf_cloud_n": (C.c_int, [_vp]),

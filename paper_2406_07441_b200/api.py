@@ -224,8 +224,10 @@ def load_cloud(path) -> PointCloud:
     return PointCloud(h.value)
 
 
-def save_cloud(cloud: PointCloud, path) -> None:
-    _check(lib.kf_cloud_save(cloud.handle, str(path).encode()))
+def save_cloud(cloud: PointCloud, path, binary=False) -> None:
+    """save_cloud (pointcloud.cpp:383-401); binary=True writes the SoA cache
+    that load_cloud recognises (bulk reads instead of the text parser)."""
+    _check((lib.kf_cloud_save_binary if binary else lib.kf_cloud_save)(cloud.handle, str(path).encode()))
 
 
 @dataclass

@@ -114,6 +114,14 @@ kf_status kf_cloud_load(const char* path, kf_cloud** out)
     });
 }
 
+kf_status kf_cloud_save_binary(const kf_cloud* c, const char* path)
+{
+    return guarded([&] {
+        kfb::save_cloud_binary(c->c, path ? path : "");
+        return ok();
+    });
+}
+
 kf_status kf_cloud_save(const kf_cloud* c, const char* path)
 {
     return guarded([&] {

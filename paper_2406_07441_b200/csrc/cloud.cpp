@@ -570,8 +570,78 @@ Cloud cloud_from_arrays(int n, const double* x, const double* y, const int* kind
     return c;
 }
 
+// Binary SoA cloud cache: "KFCLOUD1", n, nnz (int64),
+// then x, y, nx, ny (n doubles each), kind (n int32), offsets (n+1 int32),
+// neighbour ids (nnz int32, 0-based). Read with a few bulk reads instead of
+// a line parser; the same validation as the array path (cloud_from_arrays).
+static const char kBinMagic[8] = {'K', 'F', 'C', 'L', 'O', 'U', 'D', '1'};
+
+static Cloud load_cloud_binary(const std::string& path)
+{
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw IngestError(2, "cannot open cloud file: " + path);
+    auto rd = [&](void* p, size_t bytes) {
+        if (bytes && std::fread(p, 1, bytes, f) != bytes) {
+            std::fclose(f);
+            throw IngestError(2, path + ": truncated binary cloud");
+        }
+    };
+    char magic[8];
+    rd(magic, 8);
+    long long hdr[2];
+    rd(hdr, sizeof hdr);
+    const long long n = hdr[0], nnz = hdr[1];
+    if (n <= 0 || n > (1ll << 31) - 2 || nnz < 0 || nnz > (1ll << 31) - 1) {
+        std::fclose(f);
+        throw IngestError(2, path + ": bad binary cloud header");
+    }
+    std::vector<double> x(n), y(n), nx(n), ny(n);
+    std::vector<int> kind(n), off(n + 1), idx(nnz);
+    rd(x.data(), 8 * n);
+    rd(y.data(), 8 * n);
+    rd(nx.data(), 8 * n);
+    rd(ny.data(), 8 * n);
+    rd(kind.data(), 4 * n);
+    rd(off.data(), 4 * (n + 1));
+    rd(idx.data(), 4 * nnz);
+    std::fclose(f);
+    if (off[n] != nnz) throw IngestError(2, path + ": neighbour offsets do not match the entry count");
+    return cloud_from_arrays(static_cast<int>(n), x.data(), y.data(), kind.data(), nx.data(), ny.data(),
+                             off.data(), idx.data());
+}
+
+void save_cloud_binary(const Cloud& c, const std::string& path)
+{
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IngestError(2, "cannot write cloud file: " + path);
+    const long long hdr[2] = {c.n, static_cast<long long>(c.nbr.idx.size())};
+    bool ok = std::fwrite(kBinMagic, 1, 8, f) == 8 && std::fwrite(hdr, sizeof hdr, 1, f) == 1;
+    auto wr = [&](const void* p, size_t bytes) {
+        if (ok && bytes) ok = std::fwrite(p, 1, bytes, f) == bytes;
+    };
+    wr(c.x.data(), 8 * c.x.size());
+    wr(c.y.data(), 8 * c.y.size());
+    wr(c.nx.data(), 8 * c.nx.size());
+    wr(c.ny.data(), 8 * c.ny.size());
+    std::vector<int> kind(c.kind.begin(), c.kind.end());
+    wr(kind.data(), 4 * kind.size());
+    wr(c.nbr.off.data(), 4 * c.nbr.off.size());
+    wr(c.nbr.idx.data(), 4 * c.nbr.idx.size());
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw IngestError(2, "cannot write cloud file: " + path);
+}
+
 Cloud load_cloud(const std::string& path)
 {
+    {
+        // the binary cache is recognised by its magic; anything else is the
+        // reference's text format
+        std::FILE* f = std::fopen(path.c_str(), "rb");
+        char magic[8] = {0};
+        const bool bin = f && std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, kBinMagic, 8) == 0;
+        if (f) std::fclose(f);
+        if (bin) return load_cloud_binary(path);
+    }
     std::ifstream in(path);
     if (!in) throw IngestError(2, "cannot open cloud file: " + path);
     Cloud c;

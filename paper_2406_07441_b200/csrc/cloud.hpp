@@ -74,6 +74,7 @@ Cloud generate_naca_ogrid(const std::string& digits, int n_wall, int n_radial,
                           double far_field_radius);
 Cloud load_cloud(const std::string& path);
 void save_cloud(const Cloud& c, const std::string& path);
+void save_cloud_binary(const Cloud& c, const std::string& path);  // load_cloud reads both formats
 Cloud cloud_from_arrays(int n, const double* x, const double* y, const int* kind,
                         const double* nx, const double* ny, const int* off, const int* idx);
 
