@@ -408,6 +408,15 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // A/B switch for the neighbour gathers of the gradient/residual kernels
         const char* g = std::getenv("KF_GATHER");
         gather = (g && std::string(g) == "ell") ? 0 : 1;
+        // a tile's shared memory holds its staged records (<= kHaloCap + 1 plus
+        // bank-class padding) and one 16-bit entry column per stencil slot of
+        // its widest point: clouds with hub points too wide for that run the
+        // global-gather kernels instead (same results, tests/test_gpu_tiles.py)
+        int max_deg = 0;
+        for (int pt = 0; pt < c.n; ++pt) max_deg = std::max(max_deg, c.nbr.degree(pt));
+        const size_t worst = static_cast<size_t>(kTileUnits) * sizeof(double2) * (kHaloCap + 1 + 8 * 8) +
+                             static_cast<size_t>(max_deg) * kTile * sizeof(unsigned short);
+        if (worst > kMaxTileSmem) gather = 0;
         const char* pe = std::getenv("KF_PDL");
         pdl = !(pe && std::string(pe) == "0");
     }
@@ -851,6 +860,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         for (int pn = 0; pn < n_pad; ++pn)
             if (P.perm[pn] >= 0 && !P.ghost[pn]) own.push_back(pn);
         std::stable_sort(own.begin(), own.end(), [&](int a, int b) { return code[P.perm[a]] < code[P.perm[b]]; });
+        if (!gather) own.clear();  // global-gather kernels: no tiles (one idle tile below)
         const char* to = std::getenv("KF_TILE_ORDER");
         const bool bfs = !(to && std::string(to) == "morton");
         // -- formation
