@@ -4,9 +4,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2406_07441_b200 as kf
 c = kf.generate_naca_ogrid("0012", 64, 16, 12.0)
-for env in ({}, {"KF_RES_SPLIT_MAX": "0"}, {"KF_FLUX_KERNEL": "m3"}):
-    # two-thread (small-cloud) and one-thread flux kernels, and the exact variant
-    for k in ("KF_RES_SPLIT_MAX", "KF_FLUX_KERNEL"):
+for env in ({}, {"KF_RES_SPLIT_MAX": "0"}, {"KF_FLUX_KERNEL": "m3"}, {"KF_GATHER": "ell"}):
+    # two-thread (small-cloud) and one-thread flux kernels, the exact variant,
+    # the global-gather kernels
+    for k in ("KF_RES_SPLIT_MAX", "KF_FLUX_KERNEL", "KF_GATHER"):
         os.environ.pop(k, None)
     os.environ.update(env)
     for variant in ("manish_ad", "anandh", "explicit"):
@@ -15,7 +16,7 @@ for env in ({}, {"KF_RES_SPLIT_MAX": "0"}, {"KF_FLUX_KERNEL": "m3"}):
         for parts in (1, 3):
             r = kf.Solver(c, cfg, n_parts=parts).run()
             print(env, variant, parts, len(r.iters), r.abort_reason, flush=True)
-for k in ("KF_RES_SPLIT_MAX", "KF_FLUX_KERNEL"):
+for k in ("KF_RES_SPLIT_MAX", "KF_FLUX_KERNEL", "KF_GATHER"):
     os.environ.pop(k, None)
 s = kf.Solver.for_rank(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD, n_iterations=4), 1, 0, kf.nccl_unique_id())
 print("nccl", len(s.run().iters))
