@@ -169,6 +169,10 @@ cudaGraphExec_t capture_graph(cudaStream_t st, F&& enqueue)
     return x;
 }
 
+// resident 128-thread CTAs per SM the flux kernel is register-capped for
+#ifndef KF_RES_MINB
+#define KF_RES_MINB 4
+#endif
 enum Transport : int { kSingle = 0, kInProc = 1, kNccl = 2, kHost = 3 };
 
 // staged records per tile (own points + stencil neighbours); 767 x 14 doubles
@@ -334,7 +338,7 @@ struct Solver::Impl {
             else if (res_split)
                 launch(k_residual_t2<true>, P.n_tiles, 2 * kTile, sm, P.D, gslot, 0);
             else
-                launch(k_residual_t<4, true>, P.n_tiles, kTile, sm, P.D, gslot, 0);
+                launch(k_residual_t<KF_RES_MINB, true>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             return;
         }
         if (flux_exact)
@@ -1253,7 +1257,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         ck(cudaFuncSetAttribute(k_grad_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_grad_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_t<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_t<KF_RES_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
     }
 
