@@ -230,6 +230,9 @@ struct Solver::Impl {
     std::vector<void*> owned;
     cudaStream_t s = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    // two consecutive iterations (cb, cb^1) in one graph: the first kernel of
+    // the second iteration is a programmatic dependent of the first's last
+    cudaGraphExec_t graph2[2] = {nullptr, nullptr};
     cudaGraphExec_t bench_graph = nullptr;
     int bench = 0;
     int cur = 0;  // buffer holding the current state
@@ -488,6 +491,8 @@ Solver::Impl::~Impl()
         cudaStreamDestroy(pipe.s_out);
     }
     for (auto& g : graph)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto& g : graph2)
         if (g) cudaGraphExecDestroy(g);
     if (bench_graph) cudaGraphExecDestroy(bench_graph);
     if (comm) nccl().CommDestroy(comm);
@@ -1617,6 +1622,15 @@ void Solver::Impl::build_graphs()
 {
     if (!cfg.use_graph) return;
     for (int b = 0; b < 2; ++b) graph[b] = capture_graph(s, [&] { enqueue_iteration(b, 0.0, false); });
+    if (transport == kSingle || transport == kInProc) {
+        const int saved = launches;
+        for (int b = 0; b < 2; ++b)
+            graph2[b] = capture_graph(s, [&] {
+                enqueue_iteration(b, 0.0, false);
+                enqueue_iteration(b ^ 1, 0.0, false);
+            });
+        launches = saved;
+    }
 }
 
 void Solver::Impl::upload_state(const double* host, const std::function<double4*(Part&)>& sel)
@@ -1833,6 +1847,11 @@ void Solver::iterate_async(int n)
             }
             I.cur = 1;
         } else {
+            if (I.cfg.use_graph && I.graph2[I.cur] && k + 1 < n) {
+                ck(cudaGraphLaunch(I.graph2[I.cur], I.s), "graph launch");
+                ++k;  // two iterations; the state buffer flips twice
+                continue;
+            }
             if (I.cfg.use_graph)
                 ck(cudaGraphLaunch(I.graph[I.cur], I.s), "graph launch");
             else
