@@ -230,9 +230,11 @@ struct Solver::Impl {
     std::vector<void*> owned;
     cudaStream_t s = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
-    // two consecutive iterations (cb, cb^1) in one graph: the first kernel of
-    // the second iteration is a programmatic dependent of the first's last
+    // graph_iters consecutive iterations (cb, cb^1, ...) in one graph: the
+    // first kernel of each iteration is a programmatic dependent of the
+    // previous one's last (KF_GRAPH_ITERS, default 2; even)
     cudaGraphExec_t graph2[2] = {nullptr, nullptr};
+    int graph_iters = 2;
     cudaGraphExec_t bench_graph = nullptr;
     int bench = 0;
     int cur = 0;  // buffer holding the current state
@@ -1623,11 +1625,11 @@ void Solver::Impl::build_graphs()
     if (!cfg.use_graph) return;
     for (int b = 0; b < 2; ++b) graph[b] = capture_graph(s, [&] { enqueue_iteration(b, 0.0, false); });
     if (transport == kSingle || transport == kInProc) {
+        if (const char* gi = std::getenv("KF_GRAPH_ITERS")) graph_iters = std::max(2, std::atoi(gi) & ~1);
         const int saved = launches;
         for (int b = 0; b < 2; ++b)
             graph2[b] = capture_graph(s, [&] {
-                enqueue_iteration(b, 0.0, false);
-                enqueue_iteration(b ^ 1, 0.0, false);
+                for (int k = 0; k < graph_iters; ++k) enqueue_iteration(b ^ (k & 1), 0.0, false);
             });
         launches = saved;
     }
@@ -1847,9 +1849,9 @@ void Solver::iterate_async(int n)
             }
             I.cur = 1;
         } else {
-            if (I.cfg.use_graph && I.graph2[I.cur] && k + 1 < n) {
+            if (I.cfg.use_graph && I.graph2[I.cur] && k + I.graph_iters <= n) {
                 ck(cudaGraphLaunch(I.graph2[I.cur], I.s), "graph launch");
-                ++k;  // two iterations; the state buffer flips twice
+                k += I.graph_iters - 1;  // an even number of iterations: the state buffer ends where it began
                 continue;
             }
             if (I.cfg.use_graph)
