@@ -65,12 +65,19 @@ def _worker(rank, world, port, name, q):
                                     partition=case["mode"])
         assert s.n_parts == world
         r = s.run()
-        q.put((rank, None, r.residual, r.cl, r.cd, r.abort_reason, r.final_state, s.owned_points))
+        # the C-ABI host step on this rank (only its own points are read and
+        # written: the host arrays keep the whole-cloud shape)
+        s.reset()
+        s.iterate_async(3)
+        U, dU = s.get_state(with_dU=True)
+        Us, rec = s.step_host(U, dU)
+        q.put((rank, None, r.residual, r.cl, r.cd, r.abort_reason, r.final_state, s.owned_points, Us,
+               rec.residual))
         s.close()
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - reported to the parent
         import traceback
-        q.put((rank, traceback.format_exc() + repr(e), None, None, None, None, None, None))
+        q.put((rank, traceback.format_exc() + repr(e), None, None, None, None, None, None, None, None))
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
@@ -78,7 +85,12 @@ def test_ranks_over_host_communicator_match_single(name):
     case = CASES[name]
     world = case["world"]
     c = kf.generate_naca_ogrid(*case["cloud"])
-    one = kf.Solver(c, _cfg(case["variant"], case["iters"])).run()
+    single = kf.Solver(c, _cfg(case["variant"], case["iters"]))
+    one = single.run()
+    single.reset()
+    single.iterate_async(3)
+    U3, dU3 = single.get_state(with_dU=True)
+    one_step, one_rec = single.step_host(U3, dU3)
     owner = kf.partition_plan(c, world, case["mode"])
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -90,7 +102,7 @@ def test_ranks_over_host_communicator_match_single(name):
     for p in procs:
         p.join(timeout=120)
     owned_total = 0
-    for rank, err, residual, cl, cd, reason, state, n_owned in sorted(res, key=lambda x: x[0]):
+    for rank, err, residual, cl, cd, reason, state, n_owned, step_state, step_res in sorted(res, key=lambda x: x[0]):
         assert err is None, err
         assert len(residual) == len(one.iters) and reason == one.abort_reason
         assert relmax(residual, one.residual) <= 1e-13
@@ -98,6 +110,9 @@ def test_ranks_over_host_communicator_match_single(name):
         mine = owner == rank
         assert n_owned == int(mine.sum())
         assert np.array_equal(state[mine], one.final_state[mine])
+        if len(one.iters) > 3:
+            assert np.array_equal(step_state[mine], one_step[mine])
+            assert abs(step_res - one_rec.residual) <= 1e-13 * abs(one_rec.residual)
         owned_total += n_owned
     assert owned_total == c.n()
     if name == "config1":
