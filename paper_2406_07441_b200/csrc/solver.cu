@@ -169,6 +169,10 @@ cudaGraphExec_t capture_graph(cudaStream_t st, F&& enqueue)
     return x;
 }
 
+// threads of the (single-block) finalize launch
+#ifndef KF_FIN_THREADS
+#define KF_FIN_THREADS 1024
+#endif
 // resident 128-thread CTAs per SM the flux kernel is register-capped for
 #ifndef KF_RES_MINB
 #define KF_RES_MINB 4
@@ -1615,7 +1619,7 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
             mark("finalize");
         }
     } else {
-        launch(k_finalize<false>, 1, 1024, 0, parts[0].D);
+        launch(k_finalize<false>, 1, KF_FIN_THREADS, 0, parts[0].D);
         mark("finalize");
     }
 }
