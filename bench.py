@@ -1,41 +1,39 @@
 #!/usr/bin/env python
 """Benchmark of the B200 implicit-LSKUM hot path (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1]): NACA 0012 O-grid 1280x500 (640,000
-points, radius 20), M 0.85, AoA 1 deg, modified LU-SGS with exact-AD JVPs
-(manish_ad), CFL 0.2, 3 inner gradient passes, physical BCs. A *step* is one
-fixed-point iteration (driver.cpp:218-276): q, 3 q-derivative passes, split-
-flux residual, time step + S-term + diagonal, 4 forward and 3 backward colour
-sweeps, update + BCs, residual norm and CL/CD.
-
-The reference aborts this case during iteration 22, so a
-long trajectory cannot be timed. Every timed step therefore re-runs iteration
-6 from the resident iteration-5 state (kf_bench_mode: the restart copy of U
-and dU_prev is inside the timed step).
+Workload (default: BASELINE.json configs[4], the largest single-GPU config,
+"synthetic NACA 0012 cloud >= 40M points"): NACA 0012 O-grid 10240x3920
+(40,140,800 points, radius 20), M 0.63, AoA 2 deg, modified LU-SGS with
+exact-AD JVPs (manish_ad), CFL 0.2, 3 inner gradient passes, physical BCs. A
+*step* is one fixed-point iteration (driver.cpp:218-276): q, 3 q-derivative
+passes, split-flux residual, time step + S-term + diagonal, 4 forward and 3
+backward colour sweeps, update + BCs, residual norm and CL/CD. Every timed
+step re-runs iteration 6 from the resident iteration-5 state (kf_bench_mode:
+the restart copy of U and dU_prev is inside the timed step), so each step is
+the same work; --case 2|3|4 selects the other BASELINE clouds.
 
   value : device-timed Mpoint-iter/s (CUDA events on the library stream,
           state resident in HBM), whole job over all ranks.
   e2e   : the same metric through the reference-facing C-ABI call
-          kf_step_host with pinned HOST buffers: H2D(U, dU_prev) + iteration +
-          D2H(U', dU, record) every step.
+          kf_step_host_batch with pinned HOST buffers: H2D(U, dU_prev) +
+          iteration + D2H(U', dU, record) every step; `e2e.pcie` is the
+          box's own concurrent-copy ceiling for those bytes, measured in the
+          same run.
 
-Multi-GPU (--gpus N under torchrun, one process per GPU): the domain-
-decomposed solver. The cloud grows with N (n_wall = 1280 N,
-so every GPU owns ~640,000 points: weak scaling), is cut into N angular
-wedges, and every rank solves its wedge with ghost points refreshed by grouped
-ncclSend/ncclRecv between dependent stages plus one ncclAllReduce of the
-residual/forces/abort partials per iteration. `value` is all ranks' points
-times steps over the max-over-ranks device time.
-
---parts P (single process) runs the same decomposition in-process on one GPU
-(ghosts refreshed by device copies): the partitioning overhead on one B200.
+Multi-GPU (--gpus N under torchrun, one process per GPU): STRONG scaling of
+the same config-5 cloud, cut into N angular wedges; every rank solves its
+wedge with ghost points refreshed by grouped ncclSend/ncclRecv between
+dependent stages plus one ncclAllReduce of the residual/forces/abort partials
+per iteration. `value` is the cloud's points times steps over the
+max-over-ranks device time.
 
 --impl reference times the reference's own CPU solver (oracle/_ref, all host
-threads) on the same case.
+threads) on the same case and cloud; both arms print the same `config`.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import subprocess
@@ -48,9 +46,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# BASELINE.json configs (SURVEY.md §8(d) clouds); 2 is the bench workload,
-# the others are reachable with --case for evidence runs
+# BASELINE.json configs (SURVEY.md §8(d) clouds)
 CASES = {
+    1: dict(digits="0012", n_wall=320, n_radial=120, radius=20.0, mach=0.63, aoa=2.0, cfl=0.2,
+            variant="manish_ad"),
     2: dict(digits="0012", n_wall=1280, n_radial=500, radius=20.0, mach=0.85, aoa=1.0, cfl=0.2,
             variant="manish_ad"),
     3: dict(digits="0012", n_wall=2560, n_radial=960, radius=20.0, mach=1.2, aoa=0.0, cfl=0.2,
@@ -60,16 +59,20 @@ CASES = {
     5: dict(digits="0012", n_wall=10240, n_radial=3920, radius=20.0, mach=0.63, aoa=2.0, cfl=0.2,
             variant="manish_ad"),
 }
-CASE = dict(digits="0012", n_wall=1280, n_radial=500, radius=20.0, mach=0.85, aoa=1.0, cfl=0.2,
-            variant="manish_ad")
+DEFAULT_CASE = 5
 METRIC = "Mpoint-iter/s (FP64 LU-SGS+AD) and time-to-residual-drop, NACA 0012 clouds"
 UNIT = "Mpoint-iter/s"
 WARM_ITERS = 5
-# algorithmic bytes of the flux-residual kernel per point
-# (q 32 + qx,qy 64 + xy 16 + ids 4*n_s + R 32, n_s = split entries with w != 0)
-FLUX_BYTES_FIXED = 144.0
-# whole iteration, n_inner = 3, Manish: 144 + 2x176 + 144 + 176 + 121 + 121 + 97
-ITER_BYTES_FIXED = 1155.0
+# reference arm: iterations timed per run (13 s each on config 5 at 16 cores),
+# so the whole arm (46 s of reference setup included) ends in ~3 minutes
+REF_MAX_STEPS = 8
+# SURVEY.md §8(d) algorithmic bytes per point (FP64 = 8 B, index = 4 B,
+# neighbour gathers counted as cache hits):
+FLUX_BYTES_FIXED = 144.0     # S3: q 32 + qx,qy 64 + xy 16 + R 32 (+ 4 n_s ids)
+GRAD1_BYTES_FIXED = 144.0    # S1: U 32 + xy 16 + q 32 + qx,qy 64 (+ 4 n_f)
+GRADK_BYTES_FIXED = 176.0    # S2: q 32 + qx,qy 64 + xy 16 + qx,qy 64 (+ 4 n_f)
+SWEEP_BYTES_FIXED = 176.0 + 2 * 121.0  # S4 (dt, d, S) + S5 + S6 (+ 2 x 4 n_s)
+ITER_BYTES_FIXED = 1155.0    # 144 + 2x176 + 144 + 176 + 121 + 121 + 97
 
 
 def dist_env():
@@ -80,9 +83,8 @@ def dist_env():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled DURING the timed region, through
-    NVML (pynvml, ~1 ms per query, every 5 ms) so even a short timed region
-    gets many samples; nvidia-smi as the fallback."""
+    """SM clocks + throttle reasons sampled DURING the timed region through
+    NVML (every 2 ms); nvidia-smi as the fallback."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
@@ -102,7 +104,7 @@ class ClockSampler:
 
     def _nvml(self):
         nv = self.nv
-        while not self._stop.is_set():
+        while True:
             try:
                 self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
                 self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)))
@@ -112,14 +114,15 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            self._stop.wait(0.005)
+            if self._stop.wait(0.002):
+                break
 
     def _smi(self):
         fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
                   "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                   "clocks_event_reasons.sw_power_cap")
         names = ["hw_slowdown", "sw_thermal_slowdown", "hw_thermal_slowdown", "sw_power_cap"]
-        while not self._stop.is_set():
+        while True:
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + fields,
                                       "--format=csv,noheader,nounits"], capture_output=True,
@@ -132,7 +135,8 @@ class ClockSampler:
                         self.reasons.add(nm)
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            if self._stop.wait(0.05):
+                break
 
     def start(self):
         self._t = threading.Thread(target=self._nvml if self.nv else self._smi, daemon=True)
@@ -163,100 +167,80 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def reference_cpu(n_iters_total, threads, spec=CASE):
-    """Time the reference solver (oracle/_ref, else the C restatement) on the
-    case. Returns (per-iteration seconds excluding each run's iteration 1,
-    N, kind). Runs restart from freestream before the reference's abort
-    (iteration 22) so any number of iterations can be sampled."""
+def gpu_local_cpus(index):
+    """Host cores on the GPU's NUMA node (nvmlDeviceGetCpuAffinity), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(os.sched_getaffinity(0))
+        return cpus or None
+    except Exception:
+        return None
+
+
+def workload_of(spec):
+    return (f"naca0012:{spec['n_wall']}:{spec['n_radial']}:{spec['radius']:g} M{spec['mach']} "
+            f"AoA{spec['aoa']:g} {spec['variant']} CFL{spec['cfl']} n_inner3, one fixed-point iteration")
+
+
+def config_of(spec, case, n, colours):
+    """The `config` object both arms print (identical for the same case)."""
+    return {"workload": workload_of(spec), "baseline_config": case, "points": int(n),
+            "colours": int(colours),
+            "l2": "inputs larger than L2 (per-iteration working set > 400 MB vs 126 MB L2)"}
+
+
+def spec_for(case, points=None):
+    spec = dict(CASES[case])
+    if points:
+        nw, nr = points.split(":")
+        spec["n_wall"], spec["n_radial"] = int(nw), int(nr)
+    return spec
+
+
+def _refpy():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import refpy  # checker: only the cpu_baseline / reference arm may use it
+    return refpy
+
+
+def reference_sample(spec, n_timed, threads):
+    """The reference solver (oracle/_ref, else the C restatement) on the case:
+    setup seconds, per-iteration seconds of iterations 2..n_timed+1 (runs
+    restarted from freestream before the reference's own aborts, iteration 1
+    of every run excluded), N, colours, kind."""
+    refpy = _refpy()
     kind = "reference" if refpy.ref_available() else "port"
+    t0 = time.perf_counter()
     if kind == "reference":
         refpy.Reference.num_threads(threads)
         ctx = refpy.Reference.generate(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
+        colours = int(ctx.colors().max())
     else:
         os.environ["OMP_NUM_THREADS"] = str(threads)
         import paper_2406_07441_b200 as kf
         c = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
         nb = c.nbr
         ctx = refpy.Oracle(c.x, c.y, c.kind, c.normal_x, c.normal_y, nb.offsets, nb.ids)
+        colours = int(kf.color_points(c).n_colors)
+    setup = time.perf_counter() - t0
     secs = []
-    while len(secs) < n_iters_total:
-        m = min(n_iters_total - len(secs) + 1, 20)
-        t0 = time.perf_counter()
+    while len(secs) < n_timed:
+        m = min(n_timed - len(secs) + 1, 20)
+        t1 = time.perf_counter()
         r = ctx.run(variant=spec["variant"], n_iterations=m, mach=spec["mach"], aoa_deg=spec["aoa"],
                     cfl=spec["cfl"])
-        wall = time.perf_counter() - t0
+        wall = time.perf_counter() - t1
         s = list(r.seconds[1:]) if kind == "reference" else [wall / max(len(r.residual), 1)] * (len(r.residual) - 1)
         if not s:
             break
         secs.extend(s)
-    return secs[:n_iters_total], ctx.n, kind
-
-
-def time_to_drop(kf, decades=1.0, with_cpu=True):
-    """Time to a fixed residual drop (north star; RunHistory::iterations_to_decades,
-    driver.cpp:169-178) on BASELINE config 1 (NACA 0012 320x120, M 0.63, AoA 2,
-    manish_ad, CFL 0.2): the reference reaches ~1 decade before its abort in
-    iteration 423, so 10 decades is not reachable; the drop
-    reported is `decades`. GPU: device seconds of the iterations up to the
-    drop (per-iteration globaltimer records). CPU: the reference solver's own
-    per-iteration seconds for the same iterations, all host threads."""
-    c = kf.generate_naca_ogrid("0012", 320, 120, 20.0)
-    cfg = kf.SolverConfig(variant=kf.SolverVariant.ManishAD, mach_inf=0.63, aoa_deg=2.0, cfl=0.2,
-                          n_iterations=1000)
-    s = kf.Solver(c, cfg)
-    s.run(want_state=False)  # warm-up (graphs, caches)
-    h = s.run(want_state=False)
-    k = h.iterations_to_decades(decades)
-    out = {"config": "naca0012:320:120:20 M0.63 AoA2 manish_ad CFL0.2", "decades": decades,
-           "iterations": k, "recorded_iterations": len(h.iters), "abort": h.abort_reason}
-    if k <= 0:
-        return out
-    out["gpu_seconds"] = float(sum(r.seconds for r in h.iters[:k]))
-    if with_cpu:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import refpy
-        if refpy.ref_available():
-            refpy.Reference.num_threads(cpu_cores())
-            ref = refpy.Reference.generate("0012", 320, 120, 20.0)
-            r = ref.run(variant="manish_ad", n_iterations=k, mach=0.63, aoa_deg=2.0, cfl=0.2)
-            out["cpu_seconds"] = float(np.sum(r.seconds[:k]))
-            out["cpu_kind"] = "reference"
-            out["cpu_cores"] = cpu_cores()
-            out["speedup"] = out["cpu_seconds"] / out["gpu_seconds"]
-    return out
-
-
-def shuffled(kf, c, seed=7):
-    """The same cloud under a random point numbering (kf_cloud_from_arrays
-    rebuilds split stencils, LS weights and the greedy colouring)."""
-    n = c.n()
-    # wall points keep their (surface-ordered) ids so compute_forces' loop
-    # check holds; every other point gets a random id
-    wall = np.flatnonzero(c.kind == 0)
-    rest = np.setdiff1d(np.arange(n), wall)
-    perm = np.concatenate([wall, np.random.default_rng(seed).permutation(rest)])  # new id -> old id
-    inv = np.empty(n, np.int64)
-    inv[perm] = np.arange(n)
-    nb = c.nbr
-    deg = np.diff(nb.offsets)[perm]
-    off = np.zeros(n + 1, np.int32)
-    np.cumsum(deg, out=off[1:])
-    ids = np.concatenate([inv[nb.ids[nb.offsets[o]:nb.offsets[o + 1]]] for o in perm]).astype(np.int32)
-    return kf.PointCloud.from_arrays(c.x[perm], c.y[perm], c.kind[perm].astype(np.int32), c.normal_x[perm],
-                                     c.normal_y[perm], off, ids)
-
-
-def case_for(world, points=None, case=2):
-    """The bench workload at `world` GPUs: config 2 at N=1; the cloud grows
-    with N in the wall direction (weak scaling, ~640,000 points per GPU)."""
-    spec = dict(CASES[case])
-    spec["n_wall"] = spec["n_wall"] * max(world, 1)
-    if points:
-        nw, nr = points.split(":")
-        spec["n_wall"], spec["n_radial"] = int(nw), int(nr)
-    return spec
+    n = ctx.n
+    del ctx
+    return setup, secs[:n_timed], n, colours, kind
 
 
 def run_reference_arm(args):
@@ -264,26 +248,167 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = cpu_cores()
-    spec = case_for(world, args.points, args.case)
-    secs, n, kind = reference_cpu(args.warmup + args.steps, threads, spec)
-    timed = secs[args.warmup:args.warmup + args.steps] or secs
-    total = float(np.sum(timed))
-    value = n * len(timed) / total / 1e6
+    spec = spec_for(args.case, args.points)
+    k = max(1, min(args.steps, REF_MAX_STEPS))
+    setup, secs, n, colours, kind = reference_sample(spec, k, threads)
+    total = float(np.sum(secs))
+    value = n * len(secs) / total / 1e6
+    sample = (f"{len(secs)} reference iterations of the same case and cloud (run_fixed_point through the "
+              f"reference's own API; iteration 1 of the run excluded as warm-up; at most {REF_MAX_STEPS} "
+              f"timed so the arm ends in minutes: the reference iteration is {total / len(secs):.1f} s)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": len(timed), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(timed),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (generated NACA 0012 O-grid, deterministic)",
-        "config": {"workload": f"naca0012:{spec['n_wall']}:{spec['n_radial']}:20 M{spec['mach']} "
-                               f"AoA{spec['aoa']:g} {spec['variant']} CFL{spec['cfl']}, one fixed-point iteration",
-                   "points": n, "parallelism": "cpu-openmp"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{len(timed)} reference iterations of the same case (runs restarted "
-                                   f"from freestream every <=19 iterations; iteration 1 of each run excluded)"},
+        "steps": len(secs), "warmup": 1, "ms_per_step": 1e3 * total / len(secs),
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
+        "config": config_of(spec, args.case, n, colours),
+        "parallelism": f"cpu-openmp ({threads} host threads)",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_setup_seconds": setup,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def pcie_ceiling(torch, n, step_ms, reps=3):
+    """The box's concurrent host<->device copy ceiling for one e2e step's
+    bytes: H2D of (U, dU_prev) and D2H of (U', dU) on two streams, from and to
+    pinned buffers of the step's size, timed with events (best of `reps`)."""
+    dev = torch.device("cuda")
+    hin = [torch.empty((n, 4), dtype=torch.float64).pin_memory() for _ in range(2)]
+    hout = [torch.empty((n, 4), dtype=torch.float64).pin_memory() for _ in range(2)]
+    din = [torch.empty((n, 4), dtype=torch.float64, device=dev) for _ in range(2)]
+    dout = [torch.empty((n, 4), dtype=torch.float64, device=dev) for _ in range(2)]
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    best = {}
+    for mode in ("h2d", "d2h", "both"):
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream())
+            s_in.wait_event(e0)
+            s_out.wait_event(e0)
+            if mode in ("h2d", "both"):
+                with torch.cuda.stream(s_in):
+                    for a, b in zip(din, hin):
+                        a.copy_(b, non_blocking=True)
+            if mode in ("d2h", "both"):
+                with torch.cuda.stream(s_out):
+                    for a, b in zip(hout, dout):
+                        a.copy_(b, non_blocking=True)
+            e1.record(s_in)
+            e2.record(s_out)
+            torch.cuda.synchronize()
+            ts.append(max(e0.elapsed_time(e1), e0.elapsed_time(e2)))
+        best[mode] = min(ts)
+    bytes_dir = 2 * n * 32
+    both = best["both"]
+    return {"h2d_gbs": bytes_dir / best["h2d"] / 1e6, "d2h_gbs": bytes_dir / best["d2h"] / 1e6,
+            "concurrent_ms_per_step": both,
+            "bound_value": n / (max(both, step_ms) * 1e-3) / 1e6,
+            "how": "bare H2D of 2 x (n, 4) f64 and D2H of 2 x (n, 4) f64 on two streams from/to pinned "
+                   "buffers (best of 3); bound = points / max(copy time, device step time)"}
+
+
+def profiles_for(case, name):
+    """Committed per-case ncu evidence (profiles/r02_<name>_case<k>.json)."""
+    path = os.path.join(ROOT, "profiles", f"r02_{name}_case{case}.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def time_to_drop_c1(kf, with_cpu=True, decades=1.0):
+    """North-star time to a fixed residual drop (RunHistory::iterations_to_decades,
+    driver.cpp:169-178) on BASELINE config 1 (NACA 0012 320x120, M 0.63,
+    AoA 2, manish_ad, CFL 0.2): the reference reaches ~1 decade before its
+    abort in iteration 423. GPU: device seconds of the
+    iterations up to the drop (per-iteration globaltimer records). CPU: the
+    reference's own per-iteration seconds for the same iterations, all host
+    threads. Also the drop-in wall clock of the whole run, setup included
+    (generate + kf_create + kf_run vs generate + run_fixed_point)."""
+    spec = CASES[1]
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.ManishAD, mach_inf=0.63, aoa_deg=2.0, cfl=0.2,
+                          n_iterations=1000)
+    w0 = time.perf_counter()
+    c = kf.generate_naca_ogrid("0012", spec["n_wall"], spec["n_radial"], spec["radius"])
+    s = kf.Solver(c, cfg)
+    h = s.run(want_state=True)
+    gpu_wall = time.perf_counter() - w0
+    h = s.run(want_state=False)  # warm (graphs, caches) for the device timing
+    k = h.iterations_to_decades(decades)
+    out = {"config": workload_of(spec).replace(", one fixed-point iteration", "") + ", 1000 iterations",
+           "baseline_config": 1, "decades": decades, "iterations": k, "recorded_iterations": len(h.iters),
+           "abort": h.abort_reason}
+    if k > 0:
+        out["gpu_seconds"] = float(sum(r.seconds for r in h.iters[:k]))
+    drop = {"gpu_wall_seconds": gpu_wall,
+            "gpu_call": "generate_naca_ogrid + Solver (kf_create) + run (kf_run, 1000 iterations: "
+                        f"{len(h.iters)} recorded + abort) + final state download, host wall clock"}
+    if with_cpu:
+        refpy = _refpy()
+        if refpy.ref_available():
+            refpy.Reference.num_threads(cpu_cores())
+            w0 = time.perf_counter()
+            ref = refpy.Reference.generate("0012", spec["n_wall"], spec["n_radial"], spec["radius"])
+            r = ref.run(variant="manish_ad", n_iterations=1000, mach=0.63, aoa_deg=2.0, cfl=0.2)
+            drop["cpu_wall_seconds"] = time.perf_counter() - w0
+            drop["cpu_call"] = "Reference.generate + run_fixed_point (1000 iterations), host wall clock"
+            drop["speedup"] = drop["cpu_wall_seconds"] / gpu_wall
+            drop["same_history"] = bool(len(r.residual) == len(h.iters) and r.abort_reason == h.abort_reason)
+            if k > 0:
+                out["cpu_seconds"] = float(np.sum(r.seconds[:k]))
+                out["cpu_kind"] = "reference"
+                out["cpu_cores"] = cpu_cores()
+                out["speedup"] = out["cpu_seconds"] / out["gpu_seconds"]
+    out["dropin_whole_run"] = drop
+    return out
+
+
+def time_to_drop_c4(kf, with_cpu=True, max_iters=3000):
+    """Time to the residual drop actually reached on BASELINE config 4
+    (NACA 0012 5120x1920 = 9.8M points, M 0.63, AoA 2, manish_ad, CFL 0.2):
+    10 decades are unreachable, so the run goes `max_iters`
+    iterations (or to its abort), the reached drop is rounded down to 0.1
+    decade, and the time is that of the iterations up to it
+    (iterations_to_decades, driver.cpp:169-178). CPU: the reference's measured
+    per-iteration time on the same cloud (median of 2 sampled iterations) x
+    the same iteration count -- extrapolated, since thousands of 3.3-s
+    reference iterations do not fit a bench run."""
+    spec = CASES[4]
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.ManishAD, mach_inf=spec["mach"], aoa_deg=spec["aoa"],
+                          cfl=spec["cfl"], n_iterations=max_iters)
+    c = kf.generate_naca_ogrid("0012", spec["n_wall"], spec["n_radial"], spec["radius"])
+    s = kf.Solver(c, cfg)
+    h = s.run(want_state=False)
+    res = h.residual
+    out = {"config": workload_of(spec).replace(", one fixed-point iteration", "") + f", {max_iters} iterations",
+           "baseline_config": 4, "points": c.n(), "recorded_iterations": len(h.iters),
+           "abort": h.abort_reason or None}
+    del s
+    if len(res) < 2 or not res[0] > 0:
+        return out
+    reached = float(np.log10(res[0] / np.min(res)))
+    dec = float(np.floor(reached * 10.0) / 10.0)
+    out["decades_reached"] = reached
+    out["decades"] = dec
+    k = h.iterations_to_decades(dec) if dec > 0 else 0
+    out["iterations"] = k
+    if k > 0:
+        out["gpu_seconds"] = float(sum(r.seconds for r in h.iters[:k]))
+        if with_cpu:
+            setup, secs, n, _, kind = reference_sample(spec, 2, cpu_cores())
+            per_it = float(np.median(secs))
+            out.update({"cpu_seconds": per_it * k, "cpu_seconds_per_iteration": per_it, "cpu_kind": kind,
+                        "cpu_cores": cpu_cores(), "cpu_how": f"extrapolated: {k} x the median of {len(secs)} "
+                        "measured reference iterations on the same cloud",
+                        "speedup": per_it * k / out["gpu_seconds"]})
+    return out
 
 
 def main():
@@ -293,6 +418,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip time-to-drop and drop-in legs")
     ap.add_argument("--profile-only", action="store_true",
                     help="run a few steps for ncu (no JSON line)")
     ap.add_argument("--points", default=None, help="override cloud n_wall:n_radial")
@@ -302,11 +428,8 @@ def main():
                     help="override the case's solver variant (evidence runs)")
     ap.add_argument("--ordering", type=int, default=1, choices=[0, 1, 2],
                     help="in-colour point order: 0 natural, 1 Morton (default), 2 reverse Cuthill-McKee")
-    ap.add_argument("--shuffle", action="store_true",
-                    help="randomly renumber the cloud's points first (a loaded cloud with no locality: "
-                         "the --ordering demonstration)")
-    ap.add_argument("--case", type=int, default=2, choices=sorted(CASES),
-                    help="BASELINE.json config whose cloud/case to time (default 2, the bench workload)")
+    ap.add_argument("--case", type=int, default=DEFAULT_CASE, choices=sorted(CASES),
+                    help=f"BASELINE.json config whose cloud/case to time (default {DEFAULT_CASE})")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -321,23 +444,26 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    spec = case_for(world, args.points, args.case)
+    spec = spec_for(args.case, args.points)
     if args.variant:
         spec["variant"] = args.variant
 
+    t_setup = time.perf_counter()
     cloud = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
-    if args.shuffle:
-        cloud = shuffled(kf, cloud)
+    t_gen = time.perf_counter() - t_setup
     N = cloud.n()
+    colours = int(kf.color_points(cloud).n_colors)
     cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(spec["variant"]), mach_inf=spec["mach"],
                           aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=64, device=local,
                           ordering=args.ordering)
+    t_create = time.perf_counter()
     if world > 1:
         ids = [kf.nccl_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(ids, src=0)
         solver = kf.Solver.for_rank(cloud, cfg, world, rank, ids[0])
     else:
         solver = kf.Solver(cloud, cfg, n_parts=args.parts)
+    t_create = time.perf_counter() - t_create
     solver.reset()
     solver.iterate_async(WARM_ITERS)
     recs, st = solver.sync_records()
@@ -369,6 +495,8 @@ def main():
     t1.record(stream)
     torch.cuda.synchronize()
     clocks = sampler.stop()
+    if world > 1:
+        torch.distributed.barrier()
     ms = t0.elapsed_time(t1)
     recs, st = solver.sync_records()
     if st.code != 0:
@@ -379,13 +507,19 @@ def main():
     ms_max = float(ms_t.item())
     value = N * args.steps / (ms_max * 1e-3) / 1e6  # N: points of the whole (all-rank) cloud
     launches = solver.launches_per_iteration * args.steps
+    step_ms = ms_max / args.steps
 
-    # ---- end to end through the C ABI with pinned host buffers
+    # ---- end to end through the C ABI with pinned host buffers (allocated
+    # with the process on the GPU's NUMA node, so the pinned pages are local)
+    full_aff = os.sched_getaffinity(0)
+    local_cpus = gpu_local_cpus(local)
+    if local_cpus:
+        os.sched_setaffinity(0, local_cpus)
     Uh = torch.from_numpy(U0).pin_memory()
     dUh = torch.from_numpy(dU0).pin_memory()
     Uo = torch.empty_like(Uh).pin_memory()
     dUo = torch.empty_like(dUh).pin_memory()
-    import ctypes as C
+    del U0, dU0
     from paper_2406_07441_b200 import _lib
     rec = _lib.IterRecord()
     h = solver._h
@@ -396,20 +530,16 @@ def main():
         if s.code != 0:
             raise RuntimeError(s.reason.decode())
 
-    for _ in range(args.warmup):
+    n_sync = min(args.steps, 8)
+    for _ in range(min(args.warmup, 3)):
         e2e_step()
     torch.cuda.synchronize()
     # synchronous form: one blocking C-ABI call per step
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
-    e0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(n_sync):
         e2e_step()
-    e1.record(stream)
     torch.cuda.synchronize()
-    wall = time.perf_counter() - w0
-    sync_ms = max(e0.elapsed_time(e1), 1e3 * wall)
+    sync_ms = 1e3 * (time.perf_counter() - w0) / n_sync
     # pipelined form (kf_step_host_batch): the same steps, H2D of step k+1 and
     # D2H of step k-1 on the copy engines while step k computes
     Uos = [torch.empty_like(Uh).pin_memory() for _ in range(2)]
@@ -424,7 +554,7 @@ def main():
         if s.code != 0:
             raise RuntimeError(s.reason.decode())
 
-    batch(args.warmup)
+    batch(min(args.warmup, 3))
     torch.cuda.synchronize()
     # host wall clock around the blocking batch call; the median of three
     # batches (the PCIe-bound step varies by several % from run to run)
@@ -435,14 +565,13 @@ def main():
         torch.cuda.synchronize()
         walls.append(1e3 * (time.perf_counter() - w0))
     e2e_ms = float(np.median(walls))
-    et = torch.tensor([e2e_ms, sync_ms], device="cuda")
+    et = torch.tensor([e2e_ms, sync_ms * args.steps], device="cuda")
     if world > 1:
         torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
     e2e_value = N * args.steps / (float(et[0].item()) * 1e-3) / 1e6
     e2e_sync_value = N * args.steps / (float(et[1].item()) * 1e-3) / 1e6
     if abs(recs_b[args.steps - 1].residual - rec.residual) > 1e-12 * abs(rec.residual):
         raise RuntimeError("pipelined steps disagree with the synchronous step")
-
     if world > 1:
         # each rank moves only its own (+ghost) points across PCIe
         n_loc = solver.owned_points
@@ -452,125 +581,152 @@ def main():
     else:
         h2d_b = int(Uh.numel() * 8 + dUh.numel() * 8)
         d2h_b = int(Uo.numel() * 8 + dUo.numel() * 8 + C.sizeof(rec))
+    del Uos, dUos, Uh, dUh, Uo, dUo
+    pcie = pcie_ceiling(torch, solver.owned_points if world > 1 else N, step_ms)
+    pcie["frac"] = e2e_value / world / pcie["bound_value"] if world > 1 else e2e_value / pcie["bound_value"]
+    if local_cpus:
+        os.sched_setaffinity(0, full_aff)
+    torch.cuda.empty_cache()
 
     # ---- per-kernel profile (CUDA events between launches) for the roofline
-    prof = solver.profile_kernels(reps=5)
+    prof = solver.profile_kernels(reps=3)
     total_ms = sum(t for _, t in prof)
     agg = {}
     for name, t in prof:
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += t
-    flux_ms = agg["flux_residual"][1]
+    kms = lambda k: agg.get(k, [0, 0.0])[1]
     ls = kf.build_ls_coefficients(cloud)
     n_s = float(sum(np.count_nonzero(ls.split_w[k]) for k in ls.split_w)) / N
-    n_own = solver.owned_points  # the flux kernels of this rank's partition(s)
-    flux_bytes = n_own * (FLUX_BYTES_FIXED + 4.0 * n_s)
+    n_f = float(len(cloud.nbr.ids)) / N
+    del ls
+    n_own = solver.owned_points
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     if not hbm_peak:
         hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    achieved = flux_bytes / (flux_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "flux_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as f:
-                tj = json.load(f)
-            if tj.get("points") == N and world == 1 and args.parts == 1:
-                traffic = tj.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
     fp64_peak = kf.measure_fp64_peak(local)
-    fp64 = None
-    fpath = os.path.join(ROOT, "profiles", "flux_fp64.json")
-    if os.path.exists(fpath):
-        try:
-            with open(fpath) as f:
-                fj = json.load(f)
-            if fj.get("points") == N and world == 1 and args.parts == 1:
-                fl = float(fj["fp64_flops_per_launch"])
-                ach = fl / (flux_ms * 1e-3) / 1e12
-                fp64 = {"achieved_tflops": ach, "peak_tflops": fp64_peak, "frac": ach / fp64_peak,
-                        "flops_per_launch": fl, "source": fj.get("source"),
-                        "how": "ncu dfma*2 + dmul + dadd thread instructions of one launch / this run's "
-                               "CUDA-event kernel time; peak = measured DFMA loop (kf_measure_fp64_peak)"}
-        except Exception:
-            fp64 = None
+    single = world == 1 and args.parts == 1
+    fpj = profiles_for(args.case, "fp64") if single else None   # ncu FP64 flops per kernel
+    trj = profiles_for(args.case, "traffic") if single else None  # ncu DRAM bytes per kernel
 
-    # whole-iteration roofline: algorithmic bytes of all
-    # stages, the ncu FP64 count of all 13 launches, against the step time
-    n_f = float(len(cloud.nbr.ids)) / N
+    def kernel_roof(name, bytes_pp, launches_key):
+        ms_k = kms(launches_key)
+        if ms_k <= 0:
+            return None
+        alg = n_own * bytes_pp
+        o = {"kernel_ms": ms_k, "launches": agg[launches_key][0], "algorithmic_bytes": alg,
+             "achieved_gbs": alg / (ms_k * 1e-3) / 1e9, "hbm_frac": alg / (ms_k * 1e-3) / 1e9 / hbm_peak,
+             "share_of_step": ms_k / total_ms if total_ms else None}
+        if fpj and fpj.get("points") == N and launches_key in fpj.get("kernels", {}):
+            fl = float(fpj["kernels"][launches_key]["fp64_flops"])
+            o.update({"fp64_flops": fl, "fp64_tflops": fl / (ms_k * 1e-3) / 1e12,
+                      "fp64_frac": fl / (ms_k * 1e-3) / 1e12 / fp64_peak})
+        if trj and trj.get("points") == N and launches_key in trj.get("kernels", {}):
+            o["traffic"] = float(trj["kernels"][launches_key]["dram_bytes"])
+            o["traffic_over_alg"] = o["traffic"] / alg
+        return o
+
+    flux = kernel_roof("flux_residual", FLUX_BYTES_FIXED + 4.0 * n_s, "flux_residual")
+    fw = kernel_roof("lusgs_forward", 176.0 + 121.0 + 4.0 * n_s, "lusgs_forward")
+    bw = kernel_roof("lusgs_backward", 121.0 + 4.0 * n_s, "lusgs_backward")
+    g1 = kernel_roof("grad_pass1", GRAD1_BYTES_FIXED + 4.0 * n_f, "grad_pass1")
+    gk = kernel_roof("grad_passk", 2 * (GRADK_BYTES_FIXED + 4.0 * n_f), "grad_passk")
+    sweeps = None
+    if fw and bw:
+        sms = fw["kernel_ms"] + bw["kernel_ms"]
+        alg = fw["algorithmic_bytes"] + bw["algorithmic_bytes"]
+        sweeps = {"kernels": "k_forward x C (time step + S-term + diagonal + forward colour + hoisted JVP) "
+                             "+ k_backward x (C-1)",
+                  "kernel_ms": sms, "algorithmic_bytes": alg,
+                  "bytes_per_point": "176 + 2 x (121 + 4 n_s) (SURVEY.md 8(d) S4 + S5 + S6)",
+                  "achieved_gbs": alg / (sms * 1e-3) / 1e9, "hbm_frac": alg / (sms * 1e-3) / 1e9 / hbm_peak,
+                  "forward": fw, "backward": bw}
+        if "fp64_flops" in fw and "fp64_flops" in bw:
+            fl = fw["fp64_flops"] + bw["fp64_flops"]
+            sweeps.update({"fp64_flops": fl, "fp64_tflops": fl / (sms * 1e-3) / 1e12,
+                           "fp64_frac": fl / (sms * 1e-3) / 1e12 / fp64_peak})
+        if "traffic" in fw and "traffic" in bw:
+            sweeps["traffic"] = fw["traffic"] + bw["traffic"]
+            sweeps["traffic_over_alg"] = sweeps["traffic"] / alg
+
     iter_bytes = n_own * (ITER_BYTES_FIXED + 4.0 * (3 * n_f + 3 * n_s))
-    step_s = ms_max / args.steps * 1e-3
+    step_s = step_ms * 1e-3
     iteration = {"alg_bytes": iter_bytes, "achieved_gbs": iter_bytes / step_s / 1e9,
                  "hbm_frac": iter_bytes / step_s / 1e9 / hbm_peak,
                  "how": "SURVEY.md 8(d) B_alg per point (144+4nf | 2x 176+4nf | 144+4ns | 176 | 2x 121+4ns | 97) "
                         "x points / measured step time"}
-    ipath = os.path.join(ROOT, "profiles", "iter_fp64.json")
-    if os.path.exists(ipath) and world == 1 and args.parts == 1:
-        try:
-            with open(ipath) as f:
-                ij = json.load(f)
-            if ij.get("points") == N:
-                fl = float(ij["fp64_flops_per_iteration"])
-                t_ideal = max(iter_bytes / (hbm_peak * 1e9), fl / (fp64_peak * 1e12))
-                iteration.update({"fp64_flops": fl, "fp64_tflops": fl / step_s / 1e12,
-                                  "fp64_frac": fl / step_s / 1e12 / fp64_peak,
-                                  "t_ideal_over_t": t_ideal / step_s, "fp64_source": ij.get("source")})
-        except Exception:
-            pass
+    if fpj and fpj.get("points") == N:
+        fl = float(fpj["fp64_flops_per_iteration"])
+        t_ideal = max(iter_bytes / (hbm_peak * 1e9), fl / (fp64_peak * 1e12))
+        iteration.update({"fp64_flops": fl, "fp64_tflops": fl / step_s / 1e12,
+                          "fp64_frac": fl / step_s / 1e12 / fp64_peak,
+                          "t_ideal_over_t": t_ideal / step_s})
+
+    roofline = {
+        "bound": "hbm", "kernel": "flux_residual (k_residual_t)", "achieved": flux["achieved_gbs"],
+        "peak": hbm_peak, "unit": "GB/s", "frac": flux["hbm_frac"], "traffic": flux.get("traffic"),
+        "peak_source": peak_src,
+        "algorithmic_bytes_per_launch": flux["algorithmic_bytes"],
+        "bytes_per_point": f"144 + 4 n_s = {FLUX_BYTES_FIXED + 4 * n_s:.1f} (SURVEY.md 8(d) S3)",
+        "kernel_ms": flux["kernel_ms"], "kernel_share_of_step": flux["share_of_step"],
+        "note": "the flux kernel is FP64-pipe bound (SURVEY.md 8(d): ~3.8k FP64 ops per 208 B); its binding "
+                "roofline is `fp64`",
+        "fp64": ({"achieved_tflops": flux["fp64_tflops"], "peak_tflops": fp64_peak, "frac": flux["fp64_frac"],
+                  "flops_per_launch": flux["fp64_flops"],
+                  "how": "ncu 2 DFMA + DMUL + DADD thread instructions of one launch "
+                         f"(profiles/r02_fp64_case{args.case}.json) / this run's CUDA-event kernel time; "
+                         "peak = measured DFMA loop (kf_measure_fp64_peak)"} if flux and "fp64_flops" in flux
+                 else None),
+        "fp64_peak_tflops_measured": fp64_peak,
+        "sweeps": sweeps,
+        "gradients": {"pass1": g1, "passk": gk},
+        "iteration": iteration,
+    }
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
-        "config": {
-            "workload": f"naca0012:{spec['n_wall']}:{spec['n_radial']}:20 M{spec['mach']} AoA{spec['aoa']:g} "
-                        f"{spec['variant']} CFL{spec['cfl']} n_inner3, one fixed-point iteration (re-run of "
-                        "iteration 6 from the resident iteration-5 state)",
-            "baseline_config": args.case,
-            "points": N, "colours": int(kf.color_points(cloud).n_colors),
-            "parallelism": (f"domain-decomposition x{world} (angular wedges, NCCL halos)" if world > 1 else
-                            f"single-gpu, {args.parts} in-process partitions" if args.parts > 1 else "single-gpu"),
-            "l2": "inputs larger than L2 (per-iteration working set > 400 MB vs 126 MB L2)",
-        },
+        "config": config_of(spec, args.case, N, colours),
+        "parallelism": (f"domain decomposition x{world} (angular wedges, NCCL halos), same cloud at every N"
+                        if world > 1 else f"single-gpu, {args.parts} in-process partitions" if args.parts > 1
+                        else "single-gpu"),
+        "step": "iteration 6 re-run from the resident iteration-5 state (restart copy inside the step)",
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                 "call": "kf_step_host_batch (C ABI, pinned host buffers; every step H2D(U, dU_prev) + "
                         "iteration + D2H(U', dU, record), copies of neighbouring steps overlapped); "
                         "host wall clock around the call",
-                "sync_value": e2e_sync_value,
                 "batches": "median of 3 timed batches of `steps` steps",
-                "sync_call": "kf_step_host, one blocking call per step"},
+                "sync_value": e2e_sync_value, "sync_call": f"kf_step_host, one blocking call per step "
+                                                           f"({n_sync} steps)",
+                "pcie": pcie,
+                "numa": ({"gpu_local_cpus": len(local_cpus), "host_cpus": len(full_aff)} if local_cpus else None)},
         "gpu_launches": launches,
         "clocks": clocks,
-        "roofline": {
-            "bound": "hbm", "kernel": "flux_residual", "achieved": achieved, "peak": hbm_peak,
-            "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
-            "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": flux_bytes,
-            "kernel_ms": flux_ms, "kernel_share_of_step": flux_ms / total_ms if total_ms else None,
-            "note": "the flux kernel is FP64-pipe bound (SURVEY.md F4); see fp64",
-            "fp64_peak_tflops_measured": fp64_peak,
-            "fp64": fp64,
-            "iteration": iteration,
-        },
+        "roofline": roofline,
         "kernels_ms": {k: {"launches": v[0], "ms": v[1]} for k, v in agg.items()},
+        "setup_seconds": {"generate": t_gen, "create": t_create},
         "check": {"residual": recs[WARM_ITERS].residual if len(recs) > WARM_ITERS else None,
                   "cl": recs[WARM_ITERS].cl if len(recs) > WARM_ITERS else None,
                   "first_order_points": recs[WARM_ITERS].first_order_points if len(recs) > WARM_ITERS else None},
     }
+    del solver, cloud
+    torch.cuda.empty_cache()
     if rank == 0 and not args.no_cpu_baseline:
-        secs, n_ref, kind = reference_cpu(8, cpu_cores(), spec)
-        secs = secs[1:] or secs
+        setup, secs, n_ref, _, kind = reference_sample(spec, 1, cpu_cores())
         line["cpu_baseline"] = {
-            "value": n_ref / float(np.median(secs)) / 1e6, "unit": UNIT, "cores": cpu_cores(),
-            "kind": kind, "sample": f"{len(secs)} iterations of the same case on the host "
-                                    "(median per-iteration time, warm-up iteration excluded)"}
-    if rank == 0 and world == 1 and args.parts == 1 and args.case == 2:
-        line["time_to_drop"] = time_to_drop(kf, 1.0, with_cpu=not args.no_cpu_baseline)
+            "value": n_ref * len(secs) / float(np.sum(secs)) / 1e6, "unit": UNIT, "cores": cpu_cores(),
+            "kind": kind, "sample": f"{len(secs)} reference iteration(s) of the same case and cloud on the "
+                                    "host (iteration 2 of a run; iteration 1 excluded as warm-up)",
+            "setup_seconds": setup}
+    if rank == 0 and single and not args.no_extras:
+        line["time_to_drop"] = time_to_drop_c1(kf, with_cpu=not args.no_cpu_baseline)
+        if args.case in (4, 5):
+            line["time_to_drop_config4"] = time_to_drop_c4(kf, with_cpu=not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

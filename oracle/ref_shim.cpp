@@ -33,6 +33,8 @@
 #include <omp.h>
 #endif
 
+#include <algorithm>
+
 #include "kinfree/coloring.hpp"
 #include "kinfree/counters.hpp"
 #include "kinfree/driver.hpp"
@@ -279,6 +281,23 @@ void kfref_colors(void* h, int* color)
 {
     const ColorAssignment& c = static_cast<RefCtx*>(h)->colors;
     for (size_t p = 0; p < c.color.size(); ++p) color[p] = c.color[p];
+}
+
+// A caller-supplied colouring (1-based): the SweepPlan run_fixed_point takes
+// (driver.hpp:104-106) rebuilt by the reference's own build_sweep_plan
+// (coloring.cpp:54-62); 0 on success, the number of invalid edges otherwise
+// (validate_coloring, coloring.cpp:64-73).
+int kfref_set_colors(void* h, const int* color)
+{
+    RefCtx* c = static_cast<RefCtx*>(h);
+    ColorAssignment a;
+    a.color.assign(color, color + c->cloud.n());
+    a.n_colors = c->cloud.n() ? *std::max_element(a.color.begin(), a.color.end()) : 0;
+    const auto bad = validate_coloring(c->cloud, a);
+    if (!bad.empty()) return static_cast<int>(bad.size());
+    c->colors = a;
+    c->plan = build_sweep_plan(c->colors);
+    return 0;
 }
 
 // ---- per-stage entry points (state arrays are 4n doubles, AoS) ----

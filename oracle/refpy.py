@@ -138,6 +138,7 @@ class Reference:
             lib.kfref_run.argtypes = [C.c_void_p, C.POINTER(_Config), C.POINTER(C.c_int), _dp, _dp, _dp, _dp, _ip, _up, _up, _dp, C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_char_p, C.c_int]
             lib.kfref_num_threads.argtypes = [C.c_int]
             lib.kfref_counters.argtypes = [_up]
+            lib.kfref_set_colors.argtypes = [C.c_void_p, _ip]
             lib.kfref_split_flux.argtypes = [_dp, C.c_int, C.c_int, _dp]
             lib.kfref_jvp_split.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_int, _dp]
             lib.kfref_jvp_full.argtypes = [_dp, _dp, C.c_int, C.c_int, _dp]
@@ -228,6 +229,13 @@ class Reference:
         c = np.zeros(self.n, np.int32)
         self._lib.kfref_colors(self._h, c)
         return c
+
+    def set_colors(self, color):
+        """Run with a caller-supplied colouring (the SweepPlan run_fixed_point
+        takes, built by the reference's build_sweep_plan)."""
+        bad = self._lib.kfref_set_colors(self._h, np.ascontiguousarray(color, np.int32))
+        if bad:
+            raise OracleError(f"invalid colouring: {bad} neighbour pairs share a colour")
 
     def save(self, path):
         e = _err()

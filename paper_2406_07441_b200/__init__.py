@@ -26,6 +26,7 @@ from .api import (  # noqa: F401
     build_ls_coefficients,
     build_sweep_plan,
     color_points,
+    color_points_device,
     device_count,
     generate_naca_ogrid,
     jvp_full,
@@ -33,6 +34,7 @@ from .api import (  # noqa: F401
     load_cloud,
     measure_fp64_peak,
     nccl_unique_id,
+    order_wall_first,
     partition_plan,
     run_fixed_point,
     save_cloud,

@@ -32,11 +32,12 @@ EXPORTED = [
     "kf_partition_plan", "kf_layout_build", "kf_layout_free", "kf_layout_sizes",
     "kf_layout_arrays", "kf_layout_send", "kf_layout_recv", "kf_create_partitioned",
     "kf_nccl_unique_id", "kf_create_rank", "kf_create_rank_host", "kf_n_parts", "kf_owned_points", "kf_step_host_batch",
-    "kf_probe_math",
+    "kf_probe_math", "kf_cloud_color_device", "kf_cloud_order_wall_first",
 ]
 
 KF_NCCL_ID_BYTES = 128
 KF_PART_ANGULAR, KF_PART_MORTON = 0, 1
+KF_COLOR_JP_HASH, KF_COLOR_JP_LDF = 0, 1
 
 
 class Status(C.Structure):
@@ -90,6 +91,8 @@ def _load():
         "kf_cloud_n": (C.c_int, [_vp]),
         "kf_cloud_n_colors": (C.c_int, [_vp]),
         "kf_cloud_set_colors": (_S, [_vp, _ip]),
+        "kf_cloud_color_device": (_S, [_vp, C.c_int, C.c_int, C.c_uint, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+        "kf_cloud_order_wall_first": (_S, [_vp, C.POINTER(C.c_int)]),
         "kf_cloud_geometry": (None, [_vp, _dp, _dp, _ip, _dp, _dp]),
         "kf_cloud_list_nnz": (C.c_long, [_vp, C.c_int]),
         "kf_cloud_list": (None, [_vp, C.c_int, _ip, _ip]),

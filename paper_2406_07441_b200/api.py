@@ -288,6 +288,29 @@ def set_colors(cloud: PointCloud, color_of) -> None:
     _check(lib.kf_cloud_set_colors(cloud.handle, np.ascontiguousarray(color_of, np.int32)))
 
 
+def color_points_device(cloud: PointCloud, mode: str = "ldf", seed: int = 1, device: int = 0) -> ColorAssignment:
+    """Sweep-ordering variant: a Jones-Plassmann
+    colouring computed on the GPU replaces the cloud's greedy colouring
+    (color_points, coloring.cpp:23-52). mode "hash" (hashed priorities) or
+    "ldf" (largest degree first). Changes the LU-SGS sweep order: a stated
+    variant, not the reference's ordering."""
+    m = {"hash": L.KF_COLOR_JP_HASH, "ldf": L.KF_COLOR_JP_LDF}[mode]
+    nc, rounds = C.c_int(), C.c_int()
+    _check(lib.kf_cloud_color_device(cloud.handle, device, m, seed, C.byref(nc), C.byref(rounds)))
+    out = color_points(cloud)
+    out.rounds = rounds.value
+    return out
+
+
+def order_wall_first(cloud: PointCloud) -> ColorAssignment:
+    """The paper's Algorithm 5 sweep order: wall, interior
+    and outer points swept as separate groups, each in its own colour order
+    (levels (kind, colour), wall < interior < outer), built from the cloud's
+    current colouring. A stated variant, not the reference's ordering."""
+    _check(lib.kf_cloud_order_wall_first(cloud.handle, None))
+    return color_points(cloud)
+
+
 # ------------------------------------------------------------------ config
 class SolverVariant(enum.IntEnum):
     Explicit = 0
@@ -553,24 +576,72 @@ class Solver:
         st = lib.kf_sync_records(self._h, recs, cap, C.byref(nd))
         return _records(recs, min(nd.value, cap)), st
 
+    def _out_f64(self, a, name):
+        """A caller-supplied output must be a writable C-contiguous float64
+        (n, 4) array: native code writes n*4 doubles through its pointer."""
+        if a is None:
+            return np.zeros((self.n, 4))
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.shape == (self.n, 4)
+                and a.flags.c_contiguous and a.flags.writeable):
+            raise ConfigError(f"{name} must be a writable C-contiguous float64 array of shape ({self.n}, 4)")
+        return a
+
+    def _in_f64(self, a, name):
+        if a is None:
+            raise ConfigError(f"{name} is required (pass zeros for the first iteration, driver.cpp:210)")
+        a = _f64(a)
+        if a.size != self.n * 4:
+            raise ConfigError(f"{name} must hold {self.n} x 4 doubles, got {a.size}")
+        return a.reshape(self.n, 4)
+
     def step_host(self, U_in, dU_prev_in, U_out=None, dU_out=None):
-        U_out = np.zeros((self.n, 4)) if U_out is None else U_out
+        U_in = self._in_f64(U_in, "U_in")
+        dU_prev_in = self._in_f64(dU_prev_in, "dU_prev_in")
+        U_out = self._out_f64(U_out, "U_out")
+        if dU_out is not None:
+            dU_out = self._out_f64(dU_out, "dU_out")
         rec = L.IterRecord()
         st = lib.kf_step_host(self._h, _ptr(U_in), _ptr(dU_prev_in), _ptr(U_out), _ptr(dU_out),
                               C.byref(rec))
         _check(st)
         return U_out, _records([rec], 1)[0]
 
+    def _batch_ptrs(self, xs, name, out):
+        """Raw pointers of a list of (n, 4) float64 buffers (numpy arrays or
+        torch tensors, e.g. pinned host memory), validated like step_host's."""
+        ptrs = []
+        for k, x in enumerate(xs):
+            if hasattr(x, "data_ptr"):  # torch tensor
+                import torch
+                ok = (x.dtype == torch.float64 and tuple(x.shape) == (self.n, 4) and x.is_contiguous()
+                      and x.device.type == "cpu")
+                if not ok:
+                    raise ConfigError(f"{name}[{k}] must be a contiguous float64 CPU tensor of shape ({self.n}, 4)")
+                ptrs.append(x.data_ptr())
+            else:
+                if out:
+                    x = self._out_f64(x, f"{name}[{k}]")
+                elif not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.shape == (self.n, 4)
+                          and x.flags.c_contiguous):
+                    raise ConfigError(f"{name}[{k}] must be a C-contiguous float64 array of shape ({self.n}, 4)")
+                ptrs.append(x.ctypes.data)
+        return ptrs
+
     def step_host_batch(self, U_in, dU_prev_in, U_out, dU_out=None):
         """len(U_in) independent host-fed steps, pipelined (kf_step_host_batch).
         Arguments are lists of (n, 4) float64 arrays (pinned for overlap);
         returns the records."""
         m = len(U_in)
+        if len(dU_prev_in) != m or len(U_out) != m or (dU_out is not None and len(dU_out) != m):
+            raise ConfigError("step_host_batch: every buffer list needs one entry per step")
         P = C.c_void_p * m
-        pa = lambda xs: P(*[x.ctypes.data if hasattr(x, "ctypes") else x.data_ptr() for x in xs])
+        pa = lambda ptrs: P(*ptrs)
         recs = (L.IterRecord * max(m, 1))()
-        st = lib.kf_step_host_batch(self._h, m, pa(U_in), pa(dU_prev_in), pa(U_out),
-                                    None if dU_out is None else pa(dU_out), recs)
+        st = lib.kf_step_host_batch(self._h, m, pa(self._batch_ptrs(U_in, "U_in", False)),
+                                    pa(self._batch_ptrs(dU_prev_in, "dU_prev_in", False)),
+                                    pa(self._batch_ptrs(U_out, "U_out", True)),
+                                    None if dU_out is None else pa(self._batch_ptrs(dU_out, "dU_out", True)),
+                                    recs)
         _check(st)
         return _records(recs, m)
 

@@ -25,6 +25,10 @@ struct kf_ctx {
     std::unique_ptr<kfb::Solver> solver;
     kf_config cfg;
     int n = 0;
+    // n_inner < 1 is not a precondition of run_fixed_point: q_derivatives
+    // throws inside iteration 1's try block (spatial.cpp:154), so the run
+    // returns diverged with that reason and no records (driver.cpp:255-262)
+    bool bad_inner = false;
 };
 
 namespace {
@@ -66,6 +70,10 @@ kf_status guarded(F&& f)
         return err(KF_RUNTIME, "unknown error");
     }
 }
+
+constexpr const char* kBadInner = "q_derivatives: n_inner must be >= 1";
+
+kf_status bad_inner_status() { return err(KF_DIVERGED, kBadInner, -1, 1); }
 
 const kfb::Csr& list_of(const kf_cloud* c, int which)
 {
@@ -178,6 +186,27 @@ kf_status kf_cloud_set_colors(kf_cloud* c, const int* color_of)
     });
 }
 
+kf_status kf_cloud_color_device(kf_cloud* c, int device, int mode, unsigned seed, int* n_colors, int* rounds)
+{
+    return guarded([&] {
+        if (mode != KF_COLOR_JP_HASH && mode != KF_COLOR_JP_LDF) return err(KF_CONFIG, "unknown colouring mode");
+        int r = 0;
+        const int nc = kfb::jones_plassmann_colors(c->c, device, mode, seed, &r);
+        if (n_colors) *n_colors = nc;
+        if (rounds) *rounds = r;
+        return ok();
+    });
+}
+
+kf_status kf_cloud_order_wall_first(kf_cloud* c, int* n_levels)
+{
+    return guarded([&] {
+        const int m = kfb::wall_first_levels(c->c);
+        if (n_levels) *n_levels = m;
+        return ok();
+    });
+}
+
 void kf_cloud_geometry(const kf_cloud* c, double* x, double* y, int* kind, double* nx, double* ny)
 {
     const kfb::Cloud& cl = c->c;
@@ -276,12 +305,16 @@ kf_status create_ctx(const kf_cloud* cloud, const kf_config* cfg, const kfb::Par
         // run_fixed_point preconditions, driver.cpp:194-201
         if (!(cfg->cfl > 0.0)) return err(KF_CONFIG, "cfl must be positive");
         if (cfg->n_iterations < 1) return err(KF_CONFIG, "n_iterations must be >= 1");
-        if (cfg->n_inner < 1) return err(KF_CONFIG, "q_derivatives: n_inner must be >= 1");
+        // the device abort key's field widths (kernels.cuh mkkey)
+        if (cfg->n_iterations >= kfb::kMaxIterations)
+            return err(KF_CONFIG, "n_iterations must be < " + std::to_string(kfb::kMaxIterations));
         if (cfg->variant < 0 || cfg->variant > 4) return err(KF_CONFIG, "unknown variant");
         if (spec.n_parts < 1) return err(KF_CONFIG, "n_parts must be >= 1");
         if (spec.mode != kfb::kPartAngular && spec.mode != kfb::kPartMorton)
             return err(KF_CONFIG, "unknown partition mode");
         const kfb::Cloud& c = cloud->c;
+        if (c.n >= kfb::kMaxPoints)
+            return err(KF_CONFIG, "clouds are limited to " + std::to_string(kfb::kMaxPoints) + " points");
         for (int p : c.flagged)
             if (c.kind[p] == kfb::kInterior)
                 return err(KF_RUNTIME, "interior point " + std::to_string(p) +
@@ -291,7 +324,10 @@ kf_status create_ctx(const kf_cloud* cloud, const kf_config* cfg, const kfb::Par
         try {
             ctx->cfg = *cfg;
             ctx->n = c.n;
-            ctx->solver.reset(new kfb::Solver(c, *cfg, spec));
+            ctx->bad_inner = cfg->n_inner < 1;
+            kf_config scfg = *cfg;
+            if (ctx->bad_inner) scfg.n_inner = 1;  // never iterated (see kf_ctx)
+            ctx->solver.reset(new kfb::Solver(c, scfg, spec));
         } catch (...) {
             delete ctx;
             throw;
@@ -451,6 +487,15 @@ kf_status kf_run(kf_ctx* ctx, kf_iter_record* records, int* n_done, double* fina
     return guarded([&] {
         std::string reason;
         int point = -1, iteration = 0;
+        if (ctx->bad_inner) {
+            // iteration 1 throws in q_derivatives: no record, the state is the
+            // initial freestream + BC state (driver.cpp:207-208,255-262)
+            ctx->solver->reset();
+            if (final_state) ctx->solver->get_state(final_state, nullptr);
+            *n_done = 0;
+            if (loop_seconds) *loop_seconds = 0.0;
+            return err(KF_DIVERGED, kBadInner, -1, 1);
+        }
         const int code = ctx->solver->run(records, n_done, final_state, loop_seconds, reason, point,
                                           iteration);
         if (code != KF_OK) return err(code, reason, point, iteration);
@@ -485,6 +530,7 @@ kf_status kf_get_state(kf_ctx* ctx, double* U, double* dU_prev)
 kf_status kf_iterate_async(kf_ctx* ctx, int n)
 {
     return guarded([&] {
+        if (ctx->bad_inner) return bad_inner_status();
         ctx->solver->iterate_async(n);
         return ok();
     });
@@ -507,6 +553,7 @@ kf_status kf_step_host(kf_ctx* ctx, const double* U_in, const double* dU_prev_in
     return guarded([&] {
         std::string reason;
         int point = -1;
+        if (ctx->bad_inner) return bad_inner_status();
         const int code = ctx->solver->step_host(U_in, dU_prev_in, U_out, dU_out, record, reason, point);
         if (code != KF_OK) return err(code, reason, point, 1);
         return ok();
@@ -519,6 +566,7 @@ kf_status kf_step_host_batch(kf_ctx* ctx, int m, const double* const* U_in, cons
     return guarded([&] {
         std::string reason;
         int point = -1;
+        if (ctx->bad_inner) return bad_inner_status();
         const int code = ctx->solver->step_host_batch(m, U_in, dU_prev_in, U_out, dU_out, records, reason, point);
         if (code != KF_OK) return err(code, reason, point, 1);
         return ok();

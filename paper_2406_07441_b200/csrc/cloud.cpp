@@ -18,6 +18,8 @@
 #include <fstream>
 #include <limits>
 
+#include <omp.h>
+
 namespace kfb {
 
 namespace {
@@ -631,6 +633,8 @@ void save_cloud_binary(const Cloud& c, const std::string& path)
     if (!ok) throw IngestError(2, "cannot write cloud file: " + path);
 }
 
+static Cloud load_cloud_text(const std::string& path);
+
 Cloud load_cloud(const std::string& path)
 {
     {
@@ -642,61 +646,185 @@ Cloud load_cloud(const std::string& path)
         if (f) std::fclose(f);
         if (bin) return load_cloud_binary(path);
     }
-    std::ifstream in(path);
-    if (!in) throw IngestError(2, "cannot open cloud file: " + path);
-    Cloud c;
-    long expected = -1;
-    int lineno = 0;
-    std::string line;
-    std::vector<int> nb;
-    auto fail = [&](const std::string& why) {
-        throw IngestError(2, path + ":" + std::to_string(lineno) + ": parse error: " + why);
-    };
-    c.nbr.off.push_back(0);
-    while (std::getline(in, line)) {
-        ++lineno;
-        const size_t first = line.find_first_not_of(" \t\r");
-        if (first == std::string::npos || line[first] == '#') continue;
-        LineScanner sc{line.c_str()};
-        if (expected < 0) {
-            if (!sc.get_long(expected) || expected <= 0) fail("bad point count header");
-            c.x.reserve(expected);
-            continue;
-        }
-        long pid;
-        double px, py;
-        int kd, nn;
-        if (!(sc.get_long(pid) && sc.get_double(px) && sc.get_double(py) && sc.get_int(kd) &&
-              sc.get_int(nn)))
-            fail("bad point record");
-        if (pid != static_cast<long>(c.x.size()) + 1)
-            fail("point index " + std::to_string(pid) + " out of order");
-        if (kd < 0 || kd > 2) fail("bad point kind " + std::to_string(kd));
-        if (nn < 0) fail("negative neighbour count");
-        nb.assign(nn, 0);
-        for (int k = 0; k < nn; ++k) {
-            long v;
-            if (!sc.get_long(v)) fail("missing neighbour id");
-            nb[k] = static_cast<int>(v - 1);
-        }
-        double vx = 0.0, vy = 0.0;
-        if (kd == kWall || kd == kOuter) {
-            if (!(sc.get_double(vx) && sc.get_double(vy))) fail("missing normal for boundary point");
-        }
-        c.x.push_back(px);
-        c.y.push_back(py);
-        c.kind.push_back(kd);
-        c.nx.push_back(vx);
-        c.ny.push_back(vy);
-        c.nbr.idx.insert(c.nbr.idx.end(), nb.begin(), nb.end());
-        c.nbr.off.push_back(static_cast<int>(c.nbr.idx.size()));
+    return load_cloud_text(path);
+}
+
+// The reference's text format (load_cloud, pointcloud.cpp:301-381), parsed in
+// parallel: the file is read whole, its lines are NUL-terminated in place
+// (so a record's fields can never run into the next line) and split into
+// contiguous per-thread ranges of records; every thread parses its records
+// into its own CSR block, and the blocks are concatenated. Errors keep the
+// reference's semantics: the first failing line in file order wins (each
+// thread stops at its first failure; the smallest line number is reported),
+// a count mismatch is reported only if no line failed, and the post-parse
+// validation reports the smallest failing point.
+static Cloud load_cloud_text(const std::string& path)
+{
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw IngestError(2, "cannot open cloud file: " + path);
+    std::fseek(f, 0, SEEK_END);
+    const long long size = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    if (size < 0) {
+        std::fclose(f);
+        throw IngestError(2, "cannot open cloud file: " + path);
     }
-    if (expected < 0) throw IngestError(2, path + ": empty cloud file");
-    if (static_cast<long>(c.x.size()) != expected)
+    std::vector<char> buf(static_cast<size_t>(size) + 1);
+    const bool rd_ok = size == 0 || std::fread(buf.data(), 1, size, f) == static_cast<size_t>(size);
+    std::fclose(f);
+    if (!rd_ok) throw IngestError(2, "cannot open cloud file: " + path);
+    buf[size] = '\n';  // (sentinel: the last line needs no newline, as with getline)
+    // ---- line starts (parallel newline scan; newlines become NULs)
+    const int nt = std::max(1, omp_get_max_threads());
+    std::vector<std::vector<long long>> nl(nt);
+#pragma omp parallel num_threads(nt)
+    {
+        const int t = omp_get_thread_num();
+        const long long lo = size * t / nt, hi = size * (t + 1) / nt;
+        for (long long k = lo; k < hi; ++k)
+            if (buf[k] == '\n') {
+                nl[t].push_back(k);
+                buf[k] = '\0';
+            }
+    }
+    std::vector<long long> start(1, 0);
+    for (auto& v : nl)
+        for (long long k : v) start.push_back(k + 1);
+    if (start.back() >= size) start.pop_back();  // no empty line after a final newline
+    buf[size] = '\0';
+    const long long n_lines = static_cast<long long>(start.size());
+    // content lines (not blank, not a comment), in file order
+    auto content = [&](long long l) {
+        const char* q = buf.data() + start[l];
+        while (*q == ' ' || *q == '\t' || *q == '\r') ++q;
+        return *q != '\0' && *q != '#';
+    };
+    long long hdr = 0;
+    while (hdr < n_lines && !content(hdr)) ++hdr;
+    if (hdr == n_lines) throw IngestError(2, path + ": empty cloud file");
+    long expected = -1;
+    {
+        LineScanner sc{buf.data() + start[hdr]};
+        if (!sc.get_long(expected) || expected <= 0)
+            throw IngestError(2, path + ":" + std::to_string(hdr + 1) + ": parse error: bad point count header");
+    }
+    std::vector<long long> rec;  // line index of each record
+    {
+        std::vector<char> isrec(n_lines, 0);
+#pragma omp parallel for schedule(static)
+        for (long long l = hdr + 1; l < n_lines; ++l) isrec[l] = content(l) ? 1 : 0;
+        rec.reserve(static_cast<size_t>(std::max(expected, 1L)));
+        for (long long l = hdr + 1; l < n_lines; ++l)
+            if (isrec[l]) rec.push_back(l);
+    }
+    const long long n_rec = static_cast<long long>(rec.size());
+    if (n_rec > std::numeric_limits<int>::max() / 2)
+        throw IngestError(2, path + ": too many points for 32-bit indexing");
+    Cloud c;
+    c.x.resize(n_rec);
+    c.y.resize(n_rec);
+    c.nx.assign(n_rec, 0.0);
+    c.ny.assign(n_rec, 0.0);
+    c.kind.assign(n_rec, 0);
+    c.nbr.off.assign(n_rec + 1, 0);
+    std::vector<std::vector<int>> ids(nt);
+    std::vector<long long> err_line(nt, std::numeric_limits<long long>::max());
+    std::vector<std::string> err_msg(nt);
+#pragma omp parallel num_threads(nt)
+    {
+        const int t = omp_get_thread_num();
+        const long long lo = n_rec * t / nt, hi = n_rec * (t + 1) / nt;
+        std::vector<int>& out = ids[t];
+        out.reserve(static_cast<size_t>((hi - lo) * 8));
+        for (long long r = lo; r < hi; ++r) {
+            const long long l = rec[r];
+            auto fail = [&](const std::string& why) {
+                err_line[t] = l + 1;
+                err_msg[t] = path + ":" + std::to_string(l + 1) + ": parse error: " + why;
+            };
+            LineScanner sc{buf.data() + start[l]};
+            long pid;
+            double px, py;
+            int kd, nn;
+            if (!(sc.get_long(pid) && sc.get_double(px) && sc.get_double(py) && sc.get_int(kd) &&
+                  sc.get_int(nn))) {
+                fail("bad point record");
+                break;
+            }
+            if (pid != r + 1) {
+                fail("point index " + std::to_string(pid) + " out of order");
+                break;
+            }
+            if (kd < 0 || kd > 2) {
+                fail("bad point kind " + std::to_string(kd));
+                break;
+            }
+            if (nn < 0) {
+                fail("negative neighbour count");
+                break;
+            }
+            bool ok = true;
+            for (int k = 0; k < nn; ++k) {
+                long v;
+                if (!sc.get_long(v)) {
+                    fail("missing neighbour id");
+                    ok = false;
+                    break;
+                }
+                out.push_back(static_cast<int>(v - 1));
+            }
+            if (!ok) break;
+            double vx = 0.0, vy = 0.0;
+            if ((kd == kWall || kd == kOuter) && !(sc.get_double(vx) && sc.get_double(vy))) {
+                fail("missing normal for boundary point");
+                break;
+            }
+            c.x[r] = px;
+            c.y[r] = py;
+            c.kind[r] = kd;
+            c.nx[r] = vx;
+            c.ny[r] = vy;
+            c.nbr.off[r + 1] = nn;
+        }
+    }
+    {
+        int first = 0;
+        for (int t = 1; t < nt; ++t)
+            if (err_line[t] < err_line[first]) first = t;
+        if (err_line[first] != std::numeric_limits<long long>::max()) throw IngestError(2, err_msg[first]);
+    }
+    if (n_rec != expected)
         throw IngestError(2, path + ": expected " + std::to_string(expected) + " points, found " +
-                                 std::to_string(c.x.size()));
-    c.n = static_cast<int>(c.x.size());
+                                 std::to_string(n_rec));
+    for (long long r = 0; r < n_rec; ++r) {
+        c.nbr.off[r + 1] += c.nbr.off[r];
+        if (c.nbr.off[r + 1] < 0) throw IngestError(2, path + ": too many neighbour entries for 32-bit offsets");
+    }
+    c.nbr.idx.resize(c.nbr.off[n_rec]);
+#pragma omp parallel num_threads(nt)
+    {
+        const int t = omp_get_thread_num();
+        const long long lo = n_rec * t / nt;
+        std::copy(ids[t].begin(), ids[t].end(), c.nbr.idx.begin() + c.nbr.off[lo]);
+    }
+    c.n = static_cast<int>(n_rec);
+    // post-parse validation in point order (pointcloud.cpp:357-376): the
+    // smallest failing point wins
+    int bad = c.n;
+    std::string bad_msg;
+#pragma omp parallel for schedule(static) reduction(min : bad)
     for (int i = 0; i < c.n; ++i) {
+        bool b = c.nbr.degree(i) < 3;
+        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1] && !b; ++k) {
+            const int q = c.nbr.idx[k];
+            b = q < 0 || q >= c.n || q == i;
+        }
+        if (!b && c.kind[i] != kInterior) b = std::fabs(std::hypot(c.nx[i], c.ny[i]) - 1.0) > 1e-6;
+        if (b) bad = std::min(bad, i);
+    }
+    // the failing point's checks in the reference's order, for its message
+    if (bad < c.n) {
+        const int i = bad;
         if (c.nbr.degree(i) < 3)
             throw IngestError(2, path + ": point " + std::to_string(i + 1) +
                                      " has fewer than 3 neighbours");

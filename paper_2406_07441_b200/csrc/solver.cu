@@ -67,10 +67,20 @@ void d2h(T* h, const T* d, size_t n, cudaStream_t s)
     if (n) ck(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
 }
 
-unsigned key_iter(unsigned long long k) { return static_cast<unsigned>(k >> 44); }
-int key_stage(unsigned long long k) { return static_cast<int>((k >> 36) & 0xff); }
+// the fields of an abort key (kernels.cuh mkkey)
+unsigned key_iter(unsigned long long k) { return static_cast<unsigned>(k >> 40); }
+int key_stage(unsigned long long k) { return static_cast<int>((k >> 32) & 0xff); }
 int key_reason(unsigned long long k) { return static_cast<int>(k & 0xf); }
-int key_point(unsigned long long k) { return static_cast<int>((k >> 4) & 0xffffffffu); }
+int key_point(unsigned long long k) { return static_cast<int>((k >> 4) & 0x0fffffffu); }
+// Does `key` abort a call that launched iterations 1..launched? Stop keys
+// (convergence / divergence, stage q of the next iteration) do not, and
+// neither does a key of a later iteration than the call ran.
+bool is_abort(unsigned long long k, int launched)
+{
+    if (k == kNoKey) return false;
+    if (key_stage(k) == ST_Q && key_reason(k) == RS_STOP) return false;
+    return static_cast<int>(key_iter(k)) <= launched;
+}
 
 // scatter/gather between reference numbering (AoS n x 4) and device order;
 // downloads skip ghosts (kind < 0), uploads fill them too
@@ -881,63 +891,104 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         if (!gather) own.clear();  // global-gather kernels: no tiles (one idle tile below)
         const char* to = std::getenv("KF_TILE_ORDER");
         const bool bfs = !(to && std::string(to) == "morton");
-        // -- formation
+        // -- formation, in parallel over fixed chunks of the Morton order
+        // (kFormChunk owned points each; a tile never spans two chunks, so
+        // the tiles do not depend on the thread count). Inside a chunk:
+        // breadth-first over the stencil graph from the first free point.
         std::vector<int> tile_pts, tile_off(1, 0);
-        tile_pts.reserve(own.size());
         {
-            std::vector<int> stamp(n_pad, -1), qstamp(n_pad, -1), fifo, added;
-            std::vector<char> taken(n_pad, 0);
-            size_t seed = 0;
-            int tcount = 0;
-            auto next_seed = [&]() {
-                while (seed < own.size() && taken[own[seed]]) ++seed;
-                return seed < own.size() ? own[seed] : -1;
-            };
-            while (next_seed() >= 0) {
-                int npts = 0, hcount = 0;
-                fifo.clear();
-                size_t head = 0;
-                while (npts < kTile) {
-                    if (head == fifo.size()) {  // region exhausted (or start): next seed
-                        const int sd = next_seed();
-                        if (sd < 0) break;
-                        qstamp[sd] = tcount;
-                        fifo.push_back(sd);
+            constexpr size_t kFormChunk = 32768;
+            const size_t n_chunks = (own.size() + kFormChunk - 1) / kFormChunk;
+            std::vector<int> chunk_pos(n_pad, -1);  // position of an owned point inside its chunk
+#pragma omp parallel for schedule(static)
+            for (long long q = 0; q < static_cast<long long>(own.size()); ++q)
+                chunk_pos[own[q]] = static_cast<int>(q % kFormChunk);
+            std::vector<std::vector<int>> cpts(n_chunks), coff(n_chunks);
+#pragma omp parallel
+            {
+                std::vector<int> qstamp(kFormChunk), fifo, added;
+                std::vector<char> taken(kFormChunk);
+                // per-tile set of staged records (open addressing, <= kHaloCap + degree)
+                constexpr int kS = 4096;
+                std::vector<int> skey(kS, -1), sused;
+                auto touch = [&](int id) {
+                    unsigned h = (static_cast<unsigned>(id) * 2654435761u) & (kS - 1);
+                    while (skey[h] != -1 && skey[h] != id) h = (h + 1) & (kS - 1);
+                    if (skey[h] == -1) {
+                        skey[h] = id;
+                        sused.push_back(static_cast<int>(h));
+                        added.push_back(static_cast<int>(h));
                     }
-                    const int pn = fifo[head++];
-                    if (taken[pn]) continue;
-                    const int o = P.perm[pn];
-                    added.clear();
-                    auto touch = [&](int id) {
-                        if (stamp[id] != tcount) {
-                            stamp[id] = tcount;
-                            added.push_back(id);
-                        }
+                };
+#pragma omp for schedule(dynamic, 1)
+                for (long long ch = 0; ch < static_cast<long long>(n_chunks); ++ch) {
+                    const size_t c0 = ch * kFormChunk, c1 = std::min(own.size(), c0 + kFormChunk);
+                    const int m = static_cast<int>(c1 - c0);
+                    std::fill(taken.begin(), taken.begin() + m, 0);
+                    std::fill(qstamp.begin(), qstamp.begin() + m, -1);
+                    std::vector<int>& tp = cpts[ch];
+                    std::vector<int>& to = coff[ch];
+                    int seed = 0, tcount = 0;
+                    auto in_chunk = [&](int pn) {
+                        const int q = chunk_pos[pn];
+                        return q >= 0 && own[c0 + q] == pn && c0 + q < c1;
                     };
-                    touch(pn);
-                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) touch(inv[c.nbr.idx[k]]);
-                    if (hcount + static_cast<int>(added.size()) > halo_cap && npts > 0) {
-                        for (int id : added) stamp[id] = -1;
-                        break;
-                    }
-                    hcount += static_cast<int>(added.size());
-                    tile_pts.push_back(pn);
-                    ++npts;
-                    taken[pn] = 1;
-                    if (!bfs) {
-                        ++seed;
-                        continue;
-                    }
-                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
-                        const int li = inv[c.nbr.idx[k]];
-                        if (li >= 0 && !P.ghost[li] && !taken[li] && qstamp[li] != tcount) {
-                            qstamp[li] = tcount;
-                            fifo.push_back(li);
+                    auto next_seed = [&]() {
+                        while (seed < m && taken[seed]) ++seed;
+                        return seed < m ? own[c0 + seed] : -1;
+                    };
+                    while (next_seed() >= 0) {
+                        int npts = 0, hcount = 0;
+                        fifo.clear();
+                        for (int h : sused) skey[h] = -1;
+                        sused.clear();
+                        size_t head = 0;
+                        while (npts < kTile) {
+                            if (head == fifo.size()) {  // region exhausted (or start): next seed
+                                const int sd = next_seed();
+                                if (sd < 0) break;
+                                qstamp[chunk_pos[sd]] = tcount;
+                                fifo.push_back(sd);
+                            }
+                            const int pn = fifo[head++];
+                            if (taken[chunk_pos[pn]]) continue;
+                            const int o = P.perm[pn];
+                            added.clear();
+                            touch(pn);
+                            for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) touch(inv[c.nbr.idx[k]]);
+                            if (hcount + static_cast<int>(added.size()) > halo_cap && npts > 0) {
+                                for (int h : added) skey[h] = -1;  // (stale sused entries are harmless)
+                                break;
+                            }
+                            hcount += static_cast<int>(added.size());
+                            tp.push_back(pn);
+                            ++npts;
+                            taken[chunk_pos[pn]] = 1;
+                            if (!bfs) {
+                                ++seed;
+                                continue;
+                            }
+                            for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
+                                const int li = inv[c.nbr.idx[k]];
+                                if (li >= 0 && !P.ghost[li] && in_chunk(li) && !taken[chunk_pos[li]] &&
+                                    qstamp[chunk_pos[li]] != tcount) {
+                                    qstamp[chunk_pos[li]] = tcount;
+                                    fifo.push_back(li);
+                                }
+                            }
                         }
+                        to.push_back(static_cast<int>(tp.size()));
+                        ++tcount;
                     }
                 }
-                tile_off.push_back(static_cast<int>(tile_pts.size()));
-                ++tcount;
+            }
+            size_t total = 0;
+            for (auto& v : cpts) total += v.size();
+            tile_pts.reserve(total);
+            for (size_t ch = 0; ch < n_chunks; ++ch) {
+                const int base = static_cast<int>(tile_pts.size());
+                tile_pts.insert(tile_pts.end(), cpts[ch].begin(), cpts[ch].end());
+                for (int e : coff[ch]) tile_off.push_back(base + e);
             }
         }
         const int n_tiles = static_cast<int>(tile_off.size()) - 1;
@@ -1908,8 +1959,10 @@ int Solver::sync_records(kf_iter_record* records, int capacity, int* n_done, std
 {
     Impl& I = *impl_;
     const Dev& D = I.p0().D;
+    int launched = 0;
     ck(cudaMemcpyAsync(I.h_status, D.status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, I.s), "D2H");
     ck(cudaMemcpyAsync(I.h_iter, D.nrec, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
+    ck(cudaMemcpyAsync(&launched, D.iter, sizeof(int), cudaMemcpyDeviceToHost, I.s), "D2H");
     ck(cudaStreamSynchronize(I.s), "sync");
     int nd = std::min(*I.h_iter, D.rec_capacity);
     if (n_done) *n_done = nd;
@@ -1924,8 +1977,7 @@ int Solver::sync_records(kf_iter_record* records, int capacity, int* n_done, std
     const unsigned long long key = *I.h_status;
     point = -1;
     iteration = 0;
-    if (key == kNoKey) return KF_OK;
-    if (key_stage(key) == ST_Q && key_reason(key) == RS_STOP) return KF_OK;
+    if (!is_abort(key, launched)) return KF_OK;
     reason = I.message(key, point, iteration);
     return KF_DIVERGED;
 }
@@ -1960,6 +2012,12 @@ int Solver::run(kf_iter_record* records, int* n_done, double* final_state, doubl
     int code = sync_records(records, total, &done, reason, point, iteration);
     if (n_done) *n_done = done;
     key = *I.h_status;
+    // a key of iteration total + 1 (the last update left a state the next
+    // q_from_conserved would reject) is not an abort of this run: the
+    // reference returns normally after its last iteration (driver.cpp:278-281)
+    if (key != kNoKey && !(key_stage(key) == ST_Q && key_reason(key) == RS_STOP) &&
+        static_cast<int>(key_iter(key)) > total)
+        key = kNoKey;
     int diverged = 0;
     ck(cudaMemcpy(&diverged, I.p0().D.diverged, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
     if (key != kNoKey && key_stage(key) == ST_Q && key_reason(key) == RS_STOP && diverged) {
@@ -2042,7 +2100,7 @@ int Solver::step_host(const double* U_in, const double* dU_in, double* U_out, do
     I.cur = 1;
     if (rec) I.fill_record(*rec, r, false);
     const unsigned long long key = *I.h_status;
-    if (key == kNoKey || (key_stage(key) == ST_Q && key_reason(key) == RS_STOP)) return KF_OK;
+    if (!is_abort(key, 1)) return KF_OK;  // (a key of iteration 2 belongs to a next step)
     int it;
     reason = I.message(key, point, it);
     return KF_DIVERGED;
@@ -2141,7 +2199,7 @@ int Solver::step_host_batch(int m, const double* const* U_in, const double* cons
     for (int k = 0; k < m; ++k) {
         if (recs) I.fill_record(recs[k], Q.hrec[k], false);
         const unsigned long long key = Q.hstat[k];
-        if (code == KF_OK && key != kNoKey && !(key_stage(key) == ST_Q && key_reason(key) == RS_STOP)) {
+        if (code == KF_OK && is_abort(key, 1)) {
             int it;
             reason = I.message(key, point, it);
             code = KF_DIVERGED;

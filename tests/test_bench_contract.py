@@ -35,3 +35,24 @@ def test_bench_help_lists_contract_flags():
     assert out.returncode == 0
     for flag in ("--gpus", "--steps", "--warmup", "--impl"):
         assert flag in out.stdout
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libkfref.so"))
+                    and not os.path.exists(os.path.join(ROOT, "oracle", "_build", "libkforacle.so")),
+                    reason="no CPU solver built")
+def test_both_arms_print_the_same_config():
+    """The driver matches the two arms by `config`: the reference arm's must
+    be exactly what bench.py's own arm prints for the same case and cloud
+    (config_of over our own ingestion of the cloud)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2406_07441_b200 as kf
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "3", "--points", "64:16"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    spec = bench.spec_for(bench.DEFAULT_CASE, "64:16")
+    c = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
+    assert line["config"] == bench.config_of(spec, bench.DEFAULT_CASE, c.n(), kf.color_points(c).n_colors)
+    assert bench.DEFAULT_CASE == 5 and bench.CASES[5]["n_wall"] * bench.CASES[5]["n_radial"] == 40140800

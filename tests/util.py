@@ -60,3 +60,22 @@ def lattice(nx_, ny_, h=0.1, x0=0.0, y0=0.0):
                         nb.append(jj * nx_ + ii)
             nbrs.append(nb)
     return pts, nbrs
+
+
+def shuffled_cloud(c, seed=7):
+    """The same cloud under a random point numbering (wall points keep their
+    surface-ordered ids, so compute_forces' loop check holds); split stencils,
+    LS weights and the greedy colouring are rebuilt by the library."""
+    n = c.n()
+    wall = np.flatnonzero(c.kind == 0)
+    rest = np.setdiff1d(np.arange(n), wall)
+    perm = np.concatenate([wall, np.random.default_rng(seed).permutation(rest)])  # new id -> old id
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    nb = c.nbr
+    deg = np.diff(nb.offsets)[perm]
+    off = np.zeros(n + 1, np.int32)
+    np.cumsum(deg, out=off[1:])
+    ids = np.concatenate([inv[nb.ids[nb.offsets[o]:nb.offsets[o + 1]]] for o in perm]).astype(np.int32)
+    return kf.PointCloud.from_arrays(c.x[perm], c.y[perm], c.kind[perm].astype(np.int32), c.normal_x[perm],
+                                     c.normal_y[perm], off, ids)
