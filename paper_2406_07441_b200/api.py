@@ -36,10 +36,14 @@ lib = L.lib
 # ------------------------------------------------------------------ errors
 class KinfreeError(RuntimeError):
     def __init__(self, status):
-        self.code = status.code
-        self.point = status.point
-        self.iteration = status.iteration
-        self.reason = status.reason.decode(errors="replace")
+        if isinstance(status, str):  # raised by the Python layer itself
+            self.code = {ConfigError: L.KF_CONFIG}.get(type(self), L.KF_RUNTIME)
+            self.point, self.iteration, self.reason = -1, 0, status
+        else:
+            self.code = status.code
+            self.point = status.point
+            self.iteration = status.iteration
+            self.reason = status.reason.decode(errors="replace")
         super().__init__(self.reason)
 
 
@@ -637,11 +641,11 @@ class Solver:
         P = C.c_void_p * m
         pa = lambda ptrs: P(*ptrs)
         recs = (L.IterRecord * max(m, 1))()
-        st = lib.kf_step_host_batch(self._h, m, pa(self._batch_ptrs(U_in, "U_in", False)),
-                                    pa(self._batch_ptrs(dU_prev_in, "dU_prev_in", False)),
-                                    pa(self._batch_ptrs(U_out, "U_out", True)),
-                                    None if dU_out is None else pa(self._batch_ptrs(dU_out, "dU_out", True)),
-                                    recs)
+        a_in = pa(self._batch_ptrs(U_in, "U_in", False))
+        a_dprev = pa(self._batch_ptrs(dU_prev_in, "dU_prev_in", False))
+        a_out = pa(self._batch_ptrs(U_out, "U_out", True))
+        a_dout = None if dU_out is None else pa(self._batch_ptrs(dU_out, "dU_out", True))
+        st = lib.kf_step_host_batch(self._h, m, a_in, a_dprev, a_out, a_dout, recs)
         _check(st)
         return _records(recs, m)
 

@@ -101,3 +101,23 @@ def test_create_rank_host_validates_arguments():
     assert st.code == _lib.KF_CONFIG and b"callback" in st.reason
     st = _lib.lib.kf_create_rank_host(c.handle, C.byref(cfg), 2, 5, 0, ex, ar, None, C.byref(h))
     assert st.code == _lib.KF_CONFIG and b"rank out of range" in st.reason
+
+
+def test_step_host_validates_buffers_before_native_code():
+    """Solver.step_host / step_host_batch check dtype, shape and contiguity of
+    the caller's arrays before any pointer reaches kf_step_host (no device
+    needed: the checks fail first)."""
+    s = object.__new__(kf.Solver)
+    s.n = 6
+    U = np.zeros((6, 4))
+    for bad in [dict(dU_prev_in=None), dict(U_in=np.zeros((5, 4))),
+                dict(U_out=np.zeros((6, 4), np.float32)), dict(U_out=np.zeros((6, 8))[:, ::2]),
+                dict(dU_out=np.zeros((6, 4), np.int64))]:
+        args = dict(U_in=U, dU_prev_in=U, U_out=None, dU_out=None)
+        args.update(bad)
+        with pytest.raises(kf.ConfigError):
+            s.step_host(**args)
+    with pytest.raises(kf.ConfigError):
+        s.step_host_batch([U], [U], [np.zeros((6, 4), np.float32)])
+    with pytest.raises(kf.ConfigError):
+        s.step_host_batch([U, U], [U], [U, U])
