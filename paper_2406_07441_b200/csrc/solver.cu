@@ -267,6 +267,7 @@ struct Solver::Impl {
     int forces_err = 0;
     int W = 0;
     bool flux_exact = false;
+    int flux_fuse = 0;
     int sweep_threads = 32;
     // two threads per point in the flux kernel (clouds of < KF_RES_SPLIT_MAX
     // points, default 200,000: a fraction of a wave of tiles, latency bound)
@@ -357,6 +358,12 @@ struct Solver::Impl {
                 launch(k_residual_t<3, false>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             else if (res_split)
                 launch(k_residual_t2<true>, P.n_tiles, 2 * kTile, sm, P.D, gslot, 0);
+            else if (flux_fuse == 4)
+                launch(k_residual_f<4>, P.n_tiles, kTile, sm, P.D, gslot, 0);
+            else if (flux_fuse == 3)
+                launch(k_residual_f<3>, P.n_tiles, kTile, sm, P.D, gslot, 0);
+            else if (flux_fuse == 2)
+                launch(k_residual_f<2>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             else
                 launch(k_residual_t<KF_RES_MINB, true>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             return;
@@ -427,6 +434,8 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // roots, 3 CTAs/SM; the parity-margin reference)
         const char* env = std::getenv("KF_FLUX_KERNEL");
         flux_exact = env && std::string(env) == "m3";
+        // pair-fused flux kernel (k_residual_f<MINB>): fuse4 / fuse3 / fuse2
+        if (env && std::string(env).rfind("fuse", 0) == 0) flux_fuse = std::atoi(env + 4);
         if (const char* st = std::getenv("KF_SWEEP_THREADS"))
             sweep_threads = std::atoi(st) == 64 ? 64 : std::atoi(st) == 128 ? kThreads : 32;
         const char* rs = std::getenv("KF_RES_SPLIT_MAX");
@@ -1324,6 +1333,9 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         ck(cudaFuncSetAttribute(k_residual_t<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<KF_RES_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_f<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_f<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        ck(cudaFuncSetAttribute(k_residual_f<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
     }
 
     for (int b = 0; b < 2; ++b) {

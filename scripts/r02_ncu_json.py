@@ -115,13 +115,19 @@ def launch(path, out):
     hdr, data = _csv_rows(path)
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     agg = collections.OrderedDict()
+    iter_keys = set()
     for d in data:
-        g = group(d[ki]) or d[ki].split("(")[0]
+        g = group(d[ki])
+        if g:
+            iter_keys.add(g)
+        g = g or d[ki].split("(")[0]
         a = agg.setdefault(g, [0, 0.0])
         a[0] += 1
         a[1] += float(d[vi].replace(",", "")) * 1e-3
-    tot = sum(v[1] for k, v in agg.items() if group(k) or k in ("grad_pass1",))
+    tot = sum(v[1] for k, v in agg.items() if k in iter_keys)
     with open(out, "w") as f:
+        f.write("ncu launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised):\n"
+                "share = fraction of the per-iteration kernels' total\n")
         f.write(f"{'kernel':40s} {'launches':>8s} {'us total':>12s} {'share':>7s}\n")
         for k, (n, us) in agg.items():
             f.write(f"{k:40s} {n:8d} {us:12.1f} {us / tot if tot else 0:7.3f}\n")
