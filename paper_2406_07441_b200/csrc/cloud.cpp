@@ -200,7 +200,7 @@ void split_stencils(Cloud& c)
     };
     for (int sl = 0; sl < 4; ++sl) {
         Csr& s = c.split[sl];
-        s.off.assign(n + 1, 0);
+        fresh(s.off, n + 1, 0);
 #pragma omp parallel for schedule(static)
         for (int p = 0; p < n; ++p) {
             int m = 0;
@@ -208,7 +208,8 @@ void split_stencils(Cloud& c)
             s.off[p + 1] = m;
         }
         for (int p = 0; p < n; ++p) s.off[p + 1] += s.off[p];
-        s.idx.assign(s.off[n], 0);
+        s.idx.clear();
+        s.idx.resize(s.off[n]);  // (every entry written below)
 #pragma omp parallel for schedule(static)
         for (int p = 0; p < n; ++p) {
             int w = s.off[p];
@@ -292,18 +293,18 @@ void split_weights(Cloud& c, int slot, bool axis_x, int p, bool& flagged)
 void ls_operators(Cloud& c)
 {
     const size_t nnz = c.nbr.idx.size();
-    c.wx.assign(nnz, 0.0);
-    c.wy.assign(nnz, 0.0);
-    c.full_class.assign(c.n, kEmpty);
+    fresh(c.wx, nnz, 0.0);
+    fresh(c.wy, nnz, 0.0);
+    fresh(c.full_class, c.n, int(kEmpty));
     for (int s = 0; s < 4; ++s) {
-        c.split_w[s].assign(c.split[s].idx.size(), 0.0);
-        c.ls_one[s].assign(c.n, 0.0);
-        c.split_class[s].assign(c.n, kEmpty);
+        fresh(c.split_w[s], c.split[s].idx.size(), 0.0);
+        fresh(c.ls_one[s], c.n, 0.0);
+        fresh(c.split_class[s], c.n, int(kEmpty));
     }
     for (int l = 0; l < 6; ++l) {
-        c.coefA[l].assign(c.n, 0.0);
-        c.coefB[l].assign(c.n, 0.0);
-        c.coefD[l].assign(c.n, 1.0);
+        fresh(c.coefA[l], c.n, 0.0);
+        fresh(c.coefB[l], c.n, 0.0);
+        fresh(c.coefD[l], c.n, 1.0);
     }
     c.flagged.clear();
     std::vector<char> flags(c.n, 0);
@@ -362,7 +363,8 @@ void greedy_colors(Cloud& c)
         }
     std::vector<long> aoff(n + 1, 0);
     for (int i = 0; i < n; ++i) aoff[i + 1] = aoff[i] + deg[i];
-    std::vector<int> adj(aoff[n]);
+    bvec<int> adj;
+    adj.resize(aoff[n]);  // (every entry written below)
     std::vector<long> pos(aoff.begin(), aoff.end() - 1);
     for (int i = 0; i < n; ++i)
         for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k) {
@@ -378,20 +380,32 @@ void greedy_colors(Cloud& c)
         std::sort(a, a + m);
         len[i] = static_cast<int>(std::unique(a, a + m) - a);
     }
-    c.color.assign(n, 0);
+    fresh(c.color, n, 0);
     if (n > 0) c.color[0] = 1;
+    // the smallest colour no neighbour holds (the reference's `used` scan,
+    // coloring.cpp:36-44): a 64-bit mask of colours 1..64, the reference's
+    // scan only when all 64 are taken
     std::vector<char> seen;
     for (int i = 0; i < n; ++i) {
         for (int t = 0; t < len[i]; ++t) {
             const int p = adj[aoff[i] + t];
             if (c.color[p] != 0) continue;
-            seen.assign(static_cast<size_t>(len[p]) + 2, 0);
+            const int* ap = adj.data() + aoff[p];
+            unsigned long long used = 0;
             for (int u = 0; u < len[p]; ++u) {
-                const int cq = c.color[adj[aoff[p] + u]];
-                if (cq > 0 && cq < static_cast<int>(seen.size())) seen[cq] = 1;
+                const int cq = c.color[ap[u]];
+                if (cq > 0 && cq <= 64) used |= 1ull << (cq - 1);
             }
-            int k = 1;
-            while (seen[k]) ++k;
+            int k = __builtin_ffsll(static_cast<long long>(~used));
+            if (k == 0) {
+                seen.assign(static_cast<size_t>(len[p]) + 2, 0);
+                for (int u = 0; u < len[p]; ++u) {
+                    const int cq = c.color[ap[u]];
+                    if (cq > 0 && cq < static_cast<int>(seen.size())) seen[cq] = 1;
+                }
+                k = 1;
+                while (seen[k]) ++k;
+            }
             c.color[p] = k;
         }
     }
@@ -478,9 +492,9 @@ Cloud generate_naca_ogrid(const std::string& digits, int n_wall, int n_radial,
     c.n = static_cast<int>(N);
     c.x.resize(N);
     c.y.resize(N);
-    c.nx.assign(N, 0.0);
-    c.ny.assign(N, 0.0);
-    c.kind.assign(N, kInterior);
+    fresh(c.nx, N, 0.0);
+    fresh(c.ny, N, 0.0);
+    fresh(c.kind, N, int(kInterior));
 
     std::vector<WallSample> wall(n_wall);
     for (int i = 0; i < n_wall; ++i) wall[i] = surface_at(shape, 2.0 * M_PI * i / n_wall);
@@ -527,7 +541,7 @@ Cloud generate_naca_ogrid(const std::string& digits, int n_wall, int n_radial,
         c.nbr.off[id + 1] = c.nbr.off[id] + ((j == 0 || j == n_radial - 1) ? 5 : 8);
     }
     if (n_radial == 1) throw IngestError(1, "degenerate O-grid");
-    c.nbr.idx.assign(c.nbr.off[N], 0);
+    c.nbr.idx.resize(c.nbr.off[N]);  // (every entry written below)
 #pragma omp parallel for schedule(static)
     for (int j = 0; j < n_radial; ++j) {
         for (int i = 0; i < n_wall; ++i) {

@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include "hostmem.hpp"
+
 namespace kfb {
 
 enum PointKindCode : int { kWall = 0, kInterior = 1, kOuter = 2 };
@@ -25,24 +27,24 @@ enum StencilClass : int { kRegular = 0, kLineX = 1, kLineY = 2, kEmpty = 3, kSin
 enum SplitSlot : int { kXpos = 0, kXneg = 1, kYpos = 2, kYneg = 3 };
 
 struct Csr {
-    std::vector<int> off;  // n+1
-    std::vector<int> idx;
+    bvec<int> off;  // n+1
+    bvec<int> idx;
     int degree(int p) const { return off[p + 1] - off[p]; }
 };
 
 struct Cloud {
     int n = 0;
-    std::vector<double> x, y, nx, ny;
-    std::vector<int> kind;
+    bvec<double> x, y, nx, ny;
+    bvec<int> kind;
     Csr nbr;
     Csr split[4];  // xpos, xneg, ypos, yneg (same order as nbr within each list)
 
     // Least-squares operators (LsCoefficients, spatial.hpp:44-57).
-    std::vector<double> wx, wy;        // per nbr entry
-    std::vector<int> full_class;       // per point
-    std::vector<double> split_w[4];    // per split entry
-    std::vector<double> ls_one[4];     // per point
-    std::vector<int> split_class[4];   // per point
+    bvec<double> wx, wy;        // per nbr entry
+    bvec<int> full_class;       // per point
+    bvec<double> split_w[4];    // per split entry
+    bvec<double> ls_one[4];     // per point
+    bvec<int> split_class[4];   // per point
     std::vector<int> flagged;          // points owning a Singular stencil
     // The same weights as per-point linear forms of the entry offset, so the
     // device can rebuild them from gathered coordinates instead of streaming
@@ -52,13 +54,13 @@ struct Cloud {
     // which is the reference's expression term for term (spatial.cpp:64-73,
     // 102-115), hence bitwise the stored weight; lists with no weights have
     // A = B = 0, D = 1.
-    std::vector<double> coefA[6], coefB[6], coefD[6];
+    bvec<double> coefA[6], coefB[6], coefD[6];
 
     // StencilReport (pointcloud.hpp:21-26)
     std::vector<int> empty_points, singular_points;
 
     // Greedy colouring (1-based), n_colors.
-    std::vector<int> color;
+    bvec<int> color;
     int n_colors = 0;
 
     std::vector<int> wall_ids, interior_ids, outer_ids;

@@ -312,7 +312,7 @@ int wall_first_levels(Cloud& c)
     int m = 0;
     for (int l = 1; l <= 3 * C; ++l)
         if (used[l]) map[l] = ++m;
-    std::vector<int> nc(n);
+    bvec<int> nc(n);
     for (int p = 0; p < n; ++p) nc[p] = map[level(p)];
     c.color.swap(nc);
     c.n_colors = m;

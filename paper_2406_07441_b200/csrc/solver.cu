@@ -267,7 +267,6 @@ struct Solver::Impl {
     int forces_err = 0;
     int W = 0;
     bool flux_exact = false;
-    int flux_fuse = 0;
     int sweep_threads = 32;
     // two threads per point in the flux kernel (clouds of < KF_RES_SPLIT_MAX
     // points, default 200,000: a fraction of a wave of tiles, latency bound)
@@ -306,6 +305,15 @@ struct Solver::Impl {
     void* h_user = nullptr;
     char* h_stage = nullptr;
     size_t h_stage_bytes = 0;
+    // setup uploads of multi-GB arrays: pageable host memory -> two pinned
+    // staging buffers (host copy of chunk k+1 overlaps the DMA of chunk k)
+    struct Uploader {
+        char* buf[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        size_t cap = 0;
+        int next = 0;
+    } upl;
+    void upload_bytes(void* d, const void* h, size_t bytes);
     double* h_red = nullptr;
     void host_exchange();
     Part& p0() { return parts[0]; }
@@ -358,12 +366,6 @@ struct Solver::Impl {
                 launch(k_residual_t<3, false>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             else if (res_split)
                 launch(k_residual_t2<true>, P.n_tiles, 2 * kTile, sm, P.D, gslot, 0);
-            else if (flux_fuse == 4)
-                launch(k_residual_f<4>, P.n_tiles, kTile, sm, P.D, gslot, 0);
-            else if (flux_fuse == 3)
-                launch(k_residual_f<3>, P.n_tiles, kTile, sm, P.D, gslot, 0);
-            else if (flux_fuse == 2)
-                launch(k_residual_f<2>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             else
                 launch(k_residual_t<KF_RES_MINB, true>, P.n_tiles, kTile, sm, P.D, gslot, 0);
             return;
@@ -434,8 +436,6 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // roots, 3 CTAs/SM; the parity-margin reference)
         const char* env = std::getenv("KF_FLUX_KERNEL");
         flux_exact = env && std::string(env) == "m3";
-        // pair-fused flux kernel (k_residual_f<MINB>): fuse4 / fuse3 / fuse2
-        if (env && std::string(env).rfind("fuse", 0) == 0) flux_fuse = std::atoi(env + 4);
         if (const char* st = std::getenv("KF_SWEEP_THREADS"))
             sweep_threads = std::atoi(st) == 64 ? 64 : std::atoi(st) == 128 ? kThreads : 32;
         const char* rs = std::getenv("KF_RES_SPLIT_MAX");
@@ -525,6 +525,10 @@ Solver::Impl::~Impl()
     if (bench_graph) cudaGraphExecDestroy(bench_graph);
     if (comm) nccl().CommDestroy(comm);
     if (h_stage) cudaFreeHost(h_stage);
+    for (int b = 0; b < 2; ++b) {
+        if (upl.buf[b]) cudaFreeHost(upl.buf[b]);
+        if (upl.ev[b]) cudaEventDestroy(upl.ev[b]);
+    }
     if (h_red) cudaFreeHost(h_red);
     for (void* p : owned) cudaFree(p);
     for (auto& P : parts)
@@ -532,6 +536,39 @@ Solver::Impl::~Impl()
     if (h_status) cudaFreeHost(h_status);
     if (h_iter) cudaFreeHost(h_iter);
     if (s) cudaStreamDestroy(s);
+}
+
+void Solver::Impl::upload_bytes(void* d, const void* h, size_t bytes)
+{
+    if (bytes < (size_t(8) << 20)) {
+        if (bytes) ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "H2D");
+        return;
+    }
+    if (!upl.cap) {
+        upl.cap = size_t(64) << 20;
+        for (int b = 0; b < 2; ++b) {
+            ck(cudaMallocHost(&upl.buf[b], upl.cap), "cudaMallocHost");
+            ck(cudaEventCreateWithFlags(&upl.ev[b], cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(upl.ev[b], s), "event");
+        }
+    }
+    const char* src = static_cast<const char*>(h);
+    char* dst = static_cast<char*>(d);
+    for (size_t off = 0; off < bytes; off += upl.cap) {
+        const size_t m = std::min(upl.cap, bytes - off);
+        const int b = upl.next;
+        upl.next ^= 1;
+        ck(cudaEventSynchronize(upl.ev[b]), "staging wait");
+        char* stg = upl.buf[b];
+        constexpr int kPieces = 16;
+#pragma omp parallel for schedule(static)
+        for (int t = 0; t < kPieces; ++t) {
+            const size_t a = m * t / kPieces, e = m * (t + 1) / kPieces;
+            std::memcpy(stg + a, src + off + a, e - a);
+        }
+        ck(cudaMemcpyAsync(dst + off, stg, m, cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaEventRecord(upl.ev[b], s), "event");
+    }
 }
 
 // Whole-cloud data every partition shares: freestream, initial state, CFL
@@ -655,13 +692,20 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
 
     lap("renumber");
     // ---- per-point static data
-    std::vector<int> orig(P.perm);
-    std::vector<signed char> kind(n_pad, -1);
-    std::vector<double> hmin(n_pad, 0.0);
-    std::vector<double4> lsone(n_pad, make_double4(0, 0, 0, 0));
-    std::vector<double2> nrm(n_pad, make_double2(0, 0));
-    std::vector<int> near_int(n_pad, -1), wslot(n_pad, -1);
-    std::vector<unsigned char> nonempty(n_pad, 0);
+    const std::vector<int>& orig = P.perm;
+    bvec<signed char> kind;
+    bvec<double> hmin;
+    bvec<double4> lsone;
+    bvec<double2> nrm;
+    bvec<int> near_int, wslot;
+    bvec<unsigned char> nonempty;
+    fresh(kind, n_pad, static_cast<signed char>(-1));
+    fresh(hmin, n_pad, 0.0);
+    fresh(lsone, n_pad, make_double4(0, 0, 0, 0));
+    fresh(nrm, n_pad, make_double2(0, 0));
+    fresh(near_int, n_pad, -1);
+    fresh(wslot, n_pad, -1);
+    fresh(nonempty, n_pad, static_cast<unsigned char>(0));
     std::vector<int> slice_off(n_slices + 1, 0);
     for (int sl = 0; sl < n_slices; ++sl) {
         int w = 0;
@@ -676,18 +720,26 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     if (n_pad > static_cast<int>(kIdMask))
         throw SolverError(KF_CONFIG, "cloud too large for 28-bit stencil entries");
     // slots past a point's degree refer to the point itself with an empty mask
-    std::vector<unsigned> e_id(n_e, 0u);
+    bvec<unsigned> e_id;
+    e_id.resize(n_e);
+#pragma omp parallel for schedule(static)
     for (int pn = 0; pn < n_pad; ++pn)
         for (size_t e = slice_off[pn >> 5] + (pn & 31); e < static_cast<size_t>(slice_off[(pn >> 5) + 1]); e += 32)
             e_id[e] = static_cast<unsigned>(pn);
     // LS linear forms in device direction order d = X+ (xneg), X- (xpos),
     // Y+ (yneg), Y- (ypos); split slot of each direction:
     const int slot_of[4] = {kXneg, kXpos, kYneg, kYpos};
-    std::vector<double4> lsf(n_pad, make_double4(0, 0, 0, 0)), lsA(n_pad, make_double4(0, 0, 0, 0)),
-        lsB(n_pad, make_double4(0, 0, 0, 0)), lsD(n_pad, make_double4(1, 1, 1, 1));
-    std::vector<double2> lsfd(n_pad, make_double2(1, 1)), xy(n_pad, make_double2(0, 0));
+    bvec<double4> lsf, lsA, lsB, lsD;
+    bvec<double2> lsfd, xy;
+    fresh(lsf, n_pad, make_double4(0, 0, 0, 0));
+    fresh(lsA, n_pad, make_double4(0, 0, 0, 0));
+    fresh(lsB, n_pad, make_double4(0, 0, 0, 0));
+    fresh(lsD, n_pad, make_double4(1, 1, 1, 1));
+    fresh(lsfd, n_pad, make_double2(1, 1));
+    fresh(xy, n_pad, make_double2(0, 0));
     auto form = [](double A, double B, double Dn, double u, double v) { return (A * u - B * v) / Dn; };
-    std::vector<unsigned char> emask(c.nbr.idx.size(), 0);  // split mask per nbr entry
+    bvec<unsigned char> emask;  // split mask per nbr entry
+    fresh(emask, c.nbr.idx.size(), static_cast<unsigned char>(0));
     // split weight of direction d (device order) of nbr entry k of global
     // point o: the linear form, bitwise the reference's weight (checked below)
     auto entry_w = [&](int o, int k, int d) {
@@ -805,7 +857,6 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     // and those the backward sweep consumes (higher colour), each in
     // gather_products' consumption order (column, then direction); sliced
     // ELL per 32-point slice (column j of lane l at off[slice] + 32 j + l)
-    std::vector<double> swv[2];
     std::vector<int> swoff[2];
     {
         std::vector<int> colour_of(n_pad, 0);
@@ -834,24 +885,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                 swoff[dir][sl + 1] = 32 * w;
             }
             for (int sl = 0; sl < n_slices; ++sl) swoff[dir][sl + 1] += swoff[dir][sl];
-            swv[dir].assign(static_cast<size_t>(swoff[dir][n_slices]), 0.0);
-            // pass 2: fill in consumption order (column, then direction)
-#pragma omp parallel for schedule(static)
-            for (int sl = 0; sl < n_slices; ++sl)
-                for (int l = 0; l < 32; ++l) {
-                    const int pn = sl * 32 + l;
-                    const int o = P.perm[pn];
-                    if (o < 0 || P.ghost[pn]) continue;
-                    size_t j = static_cast<size_t>(swoff[dir][sl]) + l;
-                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
-                        if (!consumed(pn, k)) continue;
-                        for (int d = 0; d < 4; ++d)
-                            if (emask[k] >> d & 1u) {
-                                swv[dir][j] = entry_w(o, k, d);
-                                j += 32;
-                            }
-                    }
-                }
+            // (values: k_fill_sweep_w on the device, after the upload)
         }
     }
     lap("sweep weights");
@@ -885,7 +919,8 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     std::vector<int2> tmeta;
     int h_stride = 8, e_stride = kTile;
     std::vector<unsigned short> tell;
-    std::vector<double> tw;                  // streamed split weights (residual)
+    size_t tw_len = 0;                       // streamed split weights (residual; filled on the device)
+    double* d_tw_fill = nullptr;
     std::vector<long long> twoff(1, 0);
     std::vector<double4> tlsf, tlsA, tlsB, tlsD;
     std::vector<double2> tlsfd;
@@ -1005,7 +1040,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         struct TileOut {
             std::vector<int> halo;
             std::vector<unsigned short> ent;
-            std::vector<double> w;
+            size_t nw = 0;
             int W = 0, ns = 0;
         };
         std::vector<TileOut> outs(std::max(n_tiles, 0));
@@ -1126,23 +1161,13 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                     for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) cnt += __builtin_popcount(emask[k]);
                     ww = std::max(ww, cnt);
                 }
-                O.w.assign(static_cast<size_t>(ww) * kTile, 0.0);
-                for (int t = 0; t < m; ++t) {
-                    const int o = P.perm[pts[t]];
-                    size_t j = t;
-                    for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k)
-                        for (int d = 0; d < 4; ++d)
-                            if (emask[k] >> d & 1u) {
-                                O.w[j] = entry_w(o, k, d);
-                                j += kTile;
-                            }
-                }
+                O.nw = static_cast<size_t>(ww) * kTile;  // (values: k_fill_tile_w on the device)
             }
         }
         if (!tile_error.empty()) throw SolverError(KF_CONFIG, tile_error);
         // -- concatenate
         for (int ti = 0; ti < n_tiles; ++ti) {
-            twoff.push_back(twoff.back() + static_cast<long long>(outs[ti].w.size()));
+            twoff.push_back(twoff.back() + static_cast<long long>(outs[ti].nw));
             nh_max = std::max(nh_max, outs[ti].ns);
             P.w_max = std::max(P.w_max, outs[ti].W);
         }
@@ -1154,7 +1179,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         tell.assign(static_cast<size_t>(n_tiles) * e_stride, 0);
         tmeta.resize(n_tiles);
         // + 2 rows of padding: the residual preloads two weights per entry
-        tw.resize(twoff.back() + 2 * kTile, 0.0);
+        tw_len = static_cast<size_t>(twoff.back()) + 2 * kTile;
         tpts.assign(static_cast<size_t>(n_tiles) * kTile, -1);
         tlsf.assign(tpts.size(), make_double4(0, 0, 0, 0));
         tlsfd.assign(tpts.size(), make_double2(1, 1));
@@ -1166,7 +1191,6 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             std::copy(outs[ti].halo.begin(), outs[ti].halo.end(), thalo.begin() + static_cast<size_t>(ti) * h_stride);
             std::copy(outs[ti].ent.begin(), outs[ti].ent.end(), tell.begin() + static_cast<size_t>(ti) * e_stride);
             tmeta[ti] = make_int2(outs[ti].ns, outs[ti].W);
-            std::copy(outs[ti].w.begin(), outs[ti].w.end(), tw.begin() + twoff[ti]);
             const int m = tile_off[ti + 1] - tile_off[ti];
             for (int t = 0; t < m; ++t) {
                 const int pn = tile_pts[tile_off[ti] + t];
@@ -1193,7 +1217,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             tell.assign(e_stride, 0);
             tmeta.assign(1, make_int2(0, 0));
             twoff.push_back(0);
-            tw.push_back(0.0);
+            tw_len = 1;
             P.n_tiles = 1;
         }
     }
@@ -1223,7 +1247,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     lap("halo plan");
     // ---- device buffers
     Dev& D = P.D;
-    auto up = [&](auto* d, const auto& h) { h2d(d, h.data(), h.size(), s); };
+    auto up = [&](auto* d, const auto& h) { upload_bytes(d, h.data(), h.size() * sizeof(*h.data())); };
     D.n_pad = n_pad;
     D.n_real = n;
     D.n_colors = C;
@@ -1263,29 +1287,37 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     unsigned* d_eid = dalloc<unsigned>(n_e, owned);
     up(d_eid, e_id);
     D.e_id = d_eid;
+    double* d_sw[2];
     for (int dir = 0; dir < 2; ++dir) {
-        double* d_w = dalloc<double>(swv[dir].size(), owned);
-        up(d_w, swv[dir]);
-        D.sw[dir] = d_w;
+        const size_t len = std::max<size_t>(static_cast<size_t>(swoff[dir][n_slices]), 1);
+        d_sw[dir] = dalloc<double>(len, owned);
+        ck(cudaMemsetAsync(d_sw[dir], 0, sizeof(double) * len, s), "memset");
+        D.sw[dir] = d_sw[dir];
         int* d_o = dalloc<int>(swoff[dir].size(), owned);
         up(d_o, swoff[dir]);
         D.sw_off[dir] = d_o;
     }
-    auto up4 = [&](const std::vector<double4>& h) {
+    auto up4 = [&](const auto& h) {
         double4* d = dalloc<double4>(h.size(), owned);
         up(d, h);
         return static_cast<const double4*>(d);
     };
-    auto up2 = [&](const std::vector<double2>& h) {
+    auto up2 = [&](const auto& h) {
         double2* d = dalloc<double2>(h.size(), owned);
         up(d, h);
         return static_cast<const double2*>(d);
     };
-    D.lsf = up4(lsf);
-    D.lsfd = up2(lsfd);
-    D.lsA = up4(lsA);
-    D.lsB = up4(lsB);
-    D.lsD = up4(lsD);
+    if (!gather) {  // point-order LS forms: only the global-gather kernels read them
+        D.lsf = up4(lsf);
+        D.lsfd = up2(lsfd);
+        D.lsA = up4(lsA);
+        D.lsB = up4(lsB);
+        D.lsD = up4(lsD);
+    } else {
+        D.lsf = nullptr;
+        D.lsfd = nullptr;
+        D.lsA = D.lsB = D.lsD = nullptr;
+    }
     D.xy = up2(xy);
     int* d_tiles = dalloc<int>(tiles.size(), owned);
     up(d_tiles, tiles);
@@ -1315,9 +1347,10 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         D.t_lsA = up4(tlsA);
         D.t_lsB = up4(tlsB);
         D.t_lsD = up4(tlsD);
-        double* d_tw = dalloc<double>(tw.size(), owned);
-        up(d_tw, tw);
+        double* d_tw = dalloc<double>(tw_len, owned);
+        ck(cudaMemsetAsync(d_tw, 0, sizeof(double) * tw_len, s), "memset");
         D.t_w = d_tw;
+        d_tw_fill = d_tw;
         long long* d_twoff = dalloc<long long>(twoff.size(), owned);
         up(d_twoff, twoff);
         D.t_woff = d_twoff;
@@ -1333,9 +1366,6 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         ck(cudaFuncSetAttribute(k_residual_t<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t<KF_RES_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
         ck(cudaFuncSetAttribute(k_residual_t2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_f<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_f<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        ck(cudaFuncSetAttribute(k_residual_f<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
     }
 
     for (int b = 0; b < 2; ++b) {
@@ -1343,14 +1373,30 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         D.P[b] = dalloc<PtRec>(n_pad, owned);
         ck(cudaMemsetAsync(D.U[b], 0, sizeof(double4) * n_pad, s), "memset");
     }
+    for (int b = 0; b < 2; ++b)
+        k_init_rec<<<blocks_for(8 * static_cast<size_t>(n_pad), 256), 256, 0, s>>>(D.P[b], D.xy, n_pad);
+    // LS weight streams built on the device from the forms (kernels.cuh
+    // "setup helpers"): the flux kernel's per tile, the sweeps' per point
+    if (gather && P.n_tiles > 0 && tw_len > 1)
+        k_fill_tile_w<<<P.n_tiles, kTile, 0, s>>>(D, d_tw_fill);
     {
-        std::vector<PtRec> rec(n_pad);
-        for (int pn = 0; pn < n_pad; ++pn) {
-            rec[pn] = PtRec{};
-            rec[pn].xy = xy[pn];
+        int* pos = nullptr;
+        if (gather) {
+            pos = dalloc<int>(std::max(n_pad, 1), owned);
+            const size_t nt = static_cast<size_t>(P.n_tiles) * kTile;
+            k_tile_pos<<<blocks_for(nt, 256), 256, 0, s>>>(D.t_pts, static_cast<int>(nt), pos);
         }
-        up(D.P[0], rec);
-        up(D.P[1], rec);
+        for (int dir = 0; dir < 2; ++dir)
+            if (swoff[dir][n_slices] > 0)
+                k_fill_sweep_w<<<blocks_for(static_cast<size_t>(n_pad), 128), 128, 0, s>>>(
+                    D, dir, d_sw[dir], D.sw_off[dir], pos, gather ? D.t_lsA : D.lsA, gather ? D.t_lsB : D.lsB,
+                    gather ? D.t_lsD : D.lsD);
+        ck(cudaGetLastError(), "weight fill");
+        ck(cudaStreamSynchronize(s), "weight fill");
+        if (pos) {
+            cudaFree(pos);
+            owned.erase(std::find(owned.begin(), owned.end(), static_cast<void*>(pos)));
+        }
     }
     D.R = dalloc<double4>(n_pad, owned);
     D.dUs = dalloc<double4>(n_pad, owned);
@@ -1494,6 +1540,10 @@ void Solver::Impl::host_exchange()
     for (const Msg& m : msgs) total += (m.bytes + 15) & ~size_t(15);
     if (total > h_stage_bytes) {
         if (h_stage) cudaFreeHost(h_stage);
+    for (int b = 0; b < 2; ++b) {
+        if (upl.buf[b]) cudaFreeHost(upl.buf[b]);
+        if (upl.ev[b]) cudaEventDestroy(upl.ev[b]);
+    }
         h_stage = nullptr;
         ck(cudaMallocHost(reinterpret_cast<void**>(&h_stage), std::max<size_t>(total, 16)), "cudaMallocHost");
         h_stage_bytes = std::max<size_t>(total, 16);

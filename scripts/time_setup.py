@@ -10,4 +10,7 @@ c = kf.generate_naca_ogrid("0012", nw, nr, 20.0)
 t1 = time.time()
 s = kf.Solver(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD, mach_inf=0.63, aoa_deg=2.0, n_iterations=10))
 t2 = time.time()
-print(f"points {c.n()} ingest {t1 - t0:.2f} s solver {t2 - t1:.2f} s", flush=True)
+import resource
+ru = resource.getrusage(resource.RUSAGE_SELF)
+print(f"points {c.n()} ingest {t1 - t0:.2f} s solver {t2 - t1:.2f} s (process user {ru.ru_utime:.1f} s, "
+      f"sys {ru.ru_stime:.1f} s, max rss {ru.ru_maxrss / 1e6:.1f} GB)", flush=True)

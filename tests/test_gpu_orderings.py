@@ -152,7 +152,7 @@ def test_ordering_variant_solution_level(name):
 def test_ordering_variant_keeps_the_converged_freestream_solution(name):
     """The one convergent configuration (free-stream BCs everywhere, SPEC
     acceptance #7): the converged solution is reproduced exactly."""
-    c = kf.generate_naca_ogrid("0012", 96, 33, 12.0)
+    c = kf.generate_naca_ogrid("0012", 96, 33, 20.0)
     _variant(c, name)
     s = kf.Solver(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD, mach_inf=0.63, aoa_deg=2.0, cfl=0.2,
                                      n_iterations=200, bc_mode=kf.BcMode.FreestreamAll))
