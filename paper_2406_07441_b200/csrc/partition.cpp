@@ -2,6 +2,8 @@
 #include "partition.hpp"
 
 #include <algorithm>
+#include <parallel/algorithm>
+#include <utility>
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -36,10 +38,26 @@ std::vector<uint64_t> morton_codes(const Cloud& c)
     const double y1 = *std::max_element(c.y.begin(), c.y.end());
     const double sx = x1 > x0 ? 4294967295.0 / (x1 - x0) : 0.0;
     const double sy = y1 > y0 ? 4294967295.0 / (y1 - y0) : 0.0;
+#pragma omp parallel for schedule(static)
     for (int p = 0; p < c.n; ++p)
         code[p] = spread(static_cast<uint32_t>((c.x[p] - x0) * sx)) |
                   (spread(static_cast<uint32_t>((c.y[p] - y0) * sy)) << 1);
     return code;
+}
+
+void sort_by_key(std::vector<int>& ids, const std::vector<uint64_t>& key)
+{
+    // stable by key for ascending ids == lexicographic (key, id)
+    std::vector<std::pair<uint64_t, int>> kv(ids.size());
+#pragma omp parallel for schedule(static)
+    for (long long k = 0; k < static_cast<long long>(ids.size()); ++k) kv[k] = {key[ids[k]], ids[k]};
+    if (!std::is_sorted(ids.begin(), ids.end())) {
+        std::stable_sort(kv.begin(), kv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    } else {
+        __gnu_parallel::sort(kv.begin(), kv.end());
+    }
+#pragma omp parallel for schedule(static)
+    for (long long k = 0; k < static_cast<long long>(ids.size()); ++k) ids[k] = kv[k].second;
 }
 
 std::vector<int> rcm_rank(const Cloud& c)
@@ -149,7 +167,7 @@ std::vector<int> plan_partition(const Cloud& c, int n_parts, int mode)
 }
 
 LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, int n_parts, int rank,
-                               int ordering)
+                               int ordering, const std::vector<uint64_t>* morton)
 {
     if (static_cast<int>(owner.size()) != c.n) throw std::invalid_argument("owner size mismatch");
     if (rank < 0 || rank >= n_parts) throw std::invalid_argument("rank out of range");
@@ -196,9 +214,10 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
         for (auto& m : owned)
             std::stable_sort(m.begin(), m.end(), [&](int a, int b) { return rk[a] < rk[b]; });
     } else if (ordering == 1) {
-        const std::vector<uint64_t> code = morton_codes(c);
-        for (auto& m : owned)
-            std::stable_sort(m.begin(), m.end(), [&](int a, int b) { return code[a] < code[b]; });
+        std::vector<uint64_t> own_code;
+        if (!morton) own_code = morton_codes(c);
+        const std::vector<uint64_t>& code = morton ? *morton : own_code;
+        for (auto& m : owned) sort_by_key(m, code);
     }
     // peers
     std::vector<int> is_peer(n_parts, 0);

@@ -61,6 +61,8 @@ std::vector<int> rcm_rank(const Cloud& c);
 // 1 Morton over the global
 // bounding box (the single-GPU in-colour orders).
 LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, int n_parts, int rank,
-                               int ordering);
+                               int ordering, const std::vector<uint64_t>* morton = nullptr);
+// ids (ascending or not) reordered stably by key[id], in parallel
+void sort_by_key(std::vector<int>& ids, const std::vector<uint64_t>& key);
 
 }  // namespace kfb

@@ -479,7 +479,7 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
     const bool tm = std::getenv("KF_TIME_INGEST") != nullptr;
     for (size_t k = 0; k < ranks.size(); ++k) {
         const auto t0 = std::chrono::steady_clock::now();
-        const LocalLayout L = build_local_layout(c, owner, n_rows, ranks[k], cfg.ordering);
+        const LocalLayout L = build_local_layout(c, owner, n_rows, ranks[k], cfg.ordering, &code);
         const auto t1 = std::chrono::steady_clock::now();
         parts[k].rank = ranks[k];
         pack(c, L, code, oty, otx, red_shared, parts[k]);
@@ -931,7 +931,14 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         std::vector<int> own;
         for (int pn = 0; pn < n_pad; ++pn)
             if (P.perm[pn] >= 0 && !P.ghost[pn]) own.push_back(pn);
-        std::stable_sort(own.begin(), own.end(), [&](int a, int b) { return code[P.perm[a]] < code[P.perm[b]]; });
+        {
+            // stable by the Morton code of the global point (own is ascending)
+            std::vector<uint64_t> lc(n_pad, 0);
+#pragma omp parallel for schedule(static)
+            for (int pn = 0; pn < n_pad; ++pn)
+                if (P.perm[pn] >= 0) lc[pn] = code[P.perm[pn]];
+            sort_by_key(own, lc);
+        }
         if (!gather) own.clear();  // global-gather kernels: no tiles (one idle tile below)
         const char* to = std::getenv("KF_TILE_ORDER");
         const bool bfs = !(to && std::string(to) == "morton");
@@ -1540,10 +1547,6 @@ void Solver::Impl::host_exchange()
     for (const Msg& m : msgs) total += (m.bytes + 15) & ~size_t(15);
     if (total > h_stage_bytes) {
         if (h_stage) cudaFreeHost(h_stage);
-    for (int b = 0; b < 2; ++b) {
-        if (upl.buf[b]) cudaFreeHost(upl.buf[b]);
-        if (upl.ev[b]) cudaEventDestroy(upl.ev[b]);
-    }
         h_stage = nullptr;
         ck(cudaMallocHost(reinterpret_cast<void**>(&h_stage), std::max<size_t>(total, 16)), "cudaMallocHost");
         h_stage_bytes = std::max<size_t>(total, 16);
