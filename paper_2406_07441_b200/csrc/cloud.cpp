@@ -354,24 +354,31 @@ void ls_operators(Cloud& c)
 // Greedy colouring over the symmetrised graph, coloring.cpp:7-52.
 void greedy_colors(Cloud& c)
 {
+    // symmetrised adjacency (coloring.cpp:7-21): row i = nbr(i) then the
+    // transpose entries, built in parallel (the transpose slots are taken
+    // atomically; the order is irrelevant, every row is sorted below)
     const int n = c.n;
-    std::vector<int> deg(n + 1, 0);
+    std::vector<long> deg(n, 0);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) deg[i] = c.nbr.degree(i);
+#pragma omp parallel for schedule(static)
     for (int i = 0; i < n; ++i)
-        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k) {
-            ++deg[i];
-            ++deg[c.nbr.idx[k]];
-        }
+        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k) __atomic_fetch_add(&deg[c.nbr.idx[k]], 1L, __ATOMIC_RELAXED);
     std::vector<long> aoff(n + 1, 0);
     for (int i = 0; i < n; ++i) aoff[i + 1] = aoff[i] + deg[i];
     bvec<int> adj;
     adj.resize(aoff[n]);  // (every entry written below)
-    std::vector<long> pos(aoff.begin(), aoff.end() - 1);
+    std::vector<long> pos(n);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) {
+        const int d = c.nbr.degree(i);
+        std::copy(c.nbr.idx.data() + c.nbr.off[i], c.nbr.idx.data() + c.nbr.off[i] + d, adj.data() + aoff[i]);
+        pos[i] = aoff[i] + d;
+    }
+#pragma omp parallel for schedule(static)
     for (int i = 0; i < n; ++i)
-        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k) {
-            const int q = c.nbr.idx[k];
-            adj[pos[i]++] = q;
-            adj[pos[q]++] = i;
-        }
+        for (int k = c.nbr.off[i]; k < c.nbr.off[i + 1]; ++k)
+            adj[__atomic_fetch_add(&pos[c.nbr.idx[k]], 1L, __ATOMIC_RELAXED)] = i;
     std::vector<int> len(n);
 #pragma omp parallel for schedule(static)
     for (int i = 0; i < n; ++i) {

@@ -258,7 +258,7 @@ struct Solver::Impl {
     int* dstage_i = nullptr;
     unsigned long long* h_status = nullptr;  // pinned
     int* h_iter = nullptr;                   // pinned
-    std::vector<double> h_init;              // initial state (reference order)
+    bvec<double> h_init;                     // initial state (reference order)
     double4 fsU{};
     std::vector<double> cfl_h;
     // closed-form counter terms (whole cloud)
@@ -407,6 +407,14 @@ struct Solver::Impl {
 
 Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spec) : cfg(cf)
 {
+    const bool tm_ctor = std::getenv("KF_TIME_INGEST") != nullptr;
+    auto t_ctor = std::chrono::steady_clock::now();
+    auto lap_ctor = [&](const char* what) {
+        if (!tm_ctor) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  ctor %-15s %.2f s\n", what, std::chrono::duration<double>(t - t_ctor).count());
+        t_ctor = t;
+    };
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw SolverError(KF_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
@@ -455,8 +463,10 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         const char* pe = std::getenv("KF_PDL");
         pdl = !(pe && std::string(pe) == "0");
     }
+    lap_ctor("device");
     std::vector<double> oty, otx;
     setup_globals(c, oty, otx);
+    lap_ctor("globals");
 
     const std::vector<uint64_t> code = morton_codes(c);
     std::vector<int> owner;
@@ -464,6 +474,7 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         owner.assign(c.n, 0);
     else
         owner = plan_partition(c, n_rows, spec.mode);
+    lap_ctor("morton+owner");
     double* red_shared = nullptr;
     const size_t red_len = static_cast<size_t>(W) + kRowStride * static_cast<size_t>(n_rows);
     if (transport == kInProc) {
@@ -500,7 +511,9 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         ck(cudaStreamSynchronize(s), "nccl warm-up");
     }
     ck(cudaStreamSynchronize(s), "pack sync");
+    lap_ctor("partitions");
     build_graphs();
+    lap_ctor("graphs");
 }
 
 Solver::Impl::~Impl()
@@ -613,12 +626,14 @@ void Solver::Impl::setup_globals(const Cloud& c, std::vector<double>& oty, std::
     const double fp = 1.0 / kGamma;
     const double frhoe = fp / (kGamma - 1.0) + 0.5 * frho * (fu1 * fu1 + fu2 * fu2);
     fsU = make_double4(frho, frho * fu1, frho * fu2, frhoe);
-    h_init.assign(4 * static_cast<size_t>(n), 0.0);
+    h_init.clear();
+    h_init.resize(4 * static_cast<size_t>(n));
+#pragma omp parallel for schedule(static)
     for (int p = 0; p < n; ++p) {
-        h_init[4 * p] = fsU.x;
-        h_init[4 * p + 1] = fsU.y;
-        h_init[4 * p + 2] = fsU.z;
-        h_init[4 * p + 3] = fsU.w;
+        h_init[4 * static_cast<size_t>(p)] = fsU.x;
+        h_init[4 * static_cast<size_t>(p) + 1] = fsU.y;
+        h_init[4 * static_cast<size_t>(p) + 2] = fsU.z;
+        h_init[4 * static_cast<size_t>(p) + 3] = fsU.w;
     }
     if (cfg.bc_mode == 0) {
         for (int p : c.wall_ids) {
@@ -677,7 +692,11 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     std::vector<int> inv(c.n, -1);
     P.own_gid.clear();
     P.loc_gid.clear();
+    P.own_gid.reserve(n_pad);
+    P.loc_gid.reserve(n_pad);
     std::vector<int> own_loc, loc_loc;
+    own_loc.reserve(n_pad);
+    loc_loc.reserve(n_pad);
     for (int pn = 0; pn < n_pad; ++pn) {
         const int o = P.perm[pn];
         if (o < 0) continue;
@@ -915,15 +934,15 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     // when a region runs out, each tile <= kTile points and <= kHaloCap
     // staged records; KF_TILE_ORDER=morton = plain Morton chunks. Content
     // (parallel over tiles): slots, 16-bit entries, weight stream.
-    std::vector<int> tpts, thalo;
+    bvec<int> tpts, thalo;
     std::vector<int2> tmeta;
     int h_stride = 8, e_stride = kTile;
-    std::vector<unsigned short> tell;
+    bvec<unsigned short> tell;
     size_t tw_len = 0;                       // streamed split weights (residual; filled on the device)
     double* d_tw_fill = nullptr;
     std::vector<long long> twoff(1, 0);
-    std::vector<double4> tlsf, tlsA, tlsB, tlsD;
-    std::vector<double2> tlsfd;
+    bvec<double4> tlsf, tlsA, tlsB, tlsD;
+    bvec<double2> tlsfd;
     int nh_max = 1;
     {
         int halo_cap = kHaloCap;
@@ -1182,17 +1201,17 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         // a staging batch loads up to 512 ids unconditionally
         h_stride = std::max((nh_max + 7) & ~7, 8);
         e_stride = std::max(P.w_max, 1) * kTile;
-        thalo.assign(static_cast<size_t>(n_tiles) * h_stride + 4 * kTile, 0);
-        tell.assign(static_cast<size_t>(n_tiles) * e_stride, 0);
+        fresh(thalo, static_cast<size_t>(n_tiles) * h_stride + 4 * kTile, 0);
+        fresh(tell, static_cast<size_t>(n_tiles) * e_stride, static_cast<unsigned short>(0));
         tmeta.resize(n_tiles);
         // + 2 rows of padding: the residual preloads two weights per entry
         tw_len = static_cast<size_t>(twoff.back()) + 2 * kTile;
-        tpts.assign(static_cast<size_t>(n_tiles) * kTile, -1);
-        tlsf.assign(tpts.size(), make_double4(0, 0, 0, 0));
-        tlsfd.assign(tpts.size(), make_double2(1, 1));
-        tlsA.assign(tpts.size(), make_double4(0, 0, 0, 0));
-        tlsB.assign(tpts.size(), make_double4(0, 0, 0, 0));
-        tlsD.assign(tpts.size(), make_double4(1, 1, 1, 1));
+        fresh(tpts, static_cast<size_t>(n_tiles) * kTile, -1);
+        fresh(tlsf, tpts.size(), make_double4(0, 0, 0, 0));
+        fresh(tlsfd, tpts.size(), make_double2(1, 1));
+        fresh(tlsA, tpts.size(), make_double4(0, 0, 0, 0));
+        fresh(tlsB, tpts.size(), make_double4(0, 0, 0, 0));
+        fresh(tlsD, tpts.size(), make_double4(1, 1, 1, 1));
 #pragma omp parallel for schedule(static)
         for (int ti = 0; ti < n_tiles; ++ti) {
             std::copy(outs[ti].halo.begin(), outs[ti].halo.end(), thalo.begin() + static_cast<size_t>(ti) * h_stride);
@@ -1331,7 +1350,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     D.tiles = d_tiles;
     P.n_tile_blocks = static_cast<int>(tiles.size()) / (kThreads / 32);
     {
-        auto upi = [&](const std::vector<int>& h) {
+        auto upi = [&](const auto& h) {
             int* d = dalloc<int>(h.size(), owned);
             up(d, h);
             return static_cast<const int*>(d);
