@@ -32,7 +32,7 @@ EXPORTED = [
     "kf_partition_plan", "kf_layout_build", "kf_layout_free", "kf_layout_sizes",
     "kf_layout_arrays", "kf_layout_send", "kf_layout_recv", "kf_create_partitioned",
     "kf_nccl_unique_id", "kf_create_rank", "kf_create_rank_host", "kf_n_parts", "kf_owned_points", "kf_step_host_batch",
-    "kf_probe_math", "kf_cloud_color_device", "kf_cloud_order_wall_first",
+    "kf_probe_math", "kf_cloud_color_device", "kf_cloud_order_wall_first", "kf_layout_boundary_end",
 ]
 
 KF_NCCL_ID_BYTES = 128
@@ -133,6 +133,7 @@ def _load():
         "kf_layout_sizes": (None, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                    C.POINTER(C.c_int)]),
         "kf_layout_arrays": (None, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+        "kf_layout_boundary_end": (None, [_vp, _vp]),
         "kf_layout_send": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),
         "kf_layout_recv": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_int)]),
         "kf_create_partitioned": (_S, [_vp, C.POINTER(Config), C.c_int, C.c_int, _pp]),

@@ -741,6 +741,8 @@ class LocalLayout:
         lib.kf_layout_arrays(h, _ptr(self.perm), _ptr(self.ghost), _ptr(self.gs), _ptr(self.oe),
                              _ptr(self.ge), _ptr(self.peers))
         self.peers = self.peers[:self.n_peers]
+        self.ob = np.zeros(self.n_colors, np.int32)
+        lib.kf_layout_boundary_end(h, _ptr(self.ob))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -459,6 +459,11 @@ void kf_layout_arrays(const kf_layout* L, int* perm, unsigned char* ghost, int* 
     if (peers && !l.peers.empty()) std::memcpy(peers, l.peers.data(), l.peers.size() * sizeof(int));
 }
 
+void kf_layout_boundary_end(const kf_layout* L, int* ob)
+{
+    if (ob && !L->L.ob.empty()) std::memcpy(ob, L->L.ob.data(), L->L.ob.size() * sizeof(int));
+}
+
 int kf_layout_send(const kf_layout* L, int peer_slot, int color, int* gids)
 {
     const kfb::LocalLayout& l = L->L;

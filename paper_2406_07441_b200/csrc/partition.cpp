@@ -219,6 +219,25 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
         const std::vector<uint64_t>& code = morton ? *morton : own_code;
         for (auto& m : owned) sort_by_key(m, code);
     }
+    // boundary first inside every colour (stable: the chosen order within
+    // each part). Boundary = sent to a peer OR reading a ghost (stencils
+    // need not be symmetric): the interior neither feeds nor reads the halo.
+    {
+        std::vector<char> sent(c.n, 0);
+        for (const auto& v : send_to)
+            for (int g : v) sent[g] = 1;
+        for (int p = 0; p < c.n; ++p)
+            if (owner[p] == rank)
+                for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1] && !sent[p]; ++k)
+                    if (owner[c.nbr.idx[k]] != rank) sent[p] = 1;
+        for (auto& m : owned) std::stable_partition(m.begin(), m.end(), [&](int p) { return sent[p] != 0; });
+        L.ob.assign(C, 0);
+        for (int cc = 0; cc < C; ++cc) {
+            int nb = 0;
+            for (int p : owned[cc]) nb += sent[p];
+            L.ob[cc] = nb;  // (made absolute below)
+        }
+    }
     // peers
     std::vector<int> is_peer(n_parts, 0);
     for (int g : my_ghosts) is_peer[owner[g]] = 1;
@@ -245,6 +264,7 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
     std::vector<int> inv(c.n, -1);
     for (int cc = 0; cc < C; ++cc) {
         L.gs[cc] = static_cast<int>(L.perm.size());
+        L.ob[cc] += L.gs[cc];
         for (int p : owned[cc]) {
             inv[p] = static_cast<int>(L.perm.size());
             L.perm.push_back(p);
@@ -277,6 +297,7 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
             L.ghost.push_back(0);
         }
         if (C > 0) L.oe[C - 1] = L.ge[C - 1] = 32;
+        for (int cc = 0; cc < C; ++cc) L.ob[cc] = L.gs[cc];
     }
     for (int s = 0; s < n_parts; ++s) {
         if (peer_slot[s] < 0) continue;

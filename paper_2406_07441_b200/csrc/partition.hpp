@@ -46,6 +46,11 @@ struct LocalLayout {
     std::vector<int> perm;           // local -> global (-1 = padding)
     std::vector<unsigned char> ghost;  // local index is a ghost copy
     std::vector<int> gs, oe, ge;     // per colour: block start, owned end, block end
+    // per colour: end of the boundary owned points (gs <= ob <= oe). Owned
+    // points a peer holds as ghosts come first in their colour block, so the
+    // solver can update them, start their halo exchange and update the
+    // interior [ob, oe) while it is in flight.
+    std::vector<int> ob;
     std::vector<int> peers;          // ranks exchanged with, ascending
     // per peer (index into peers) and colour
     std::vector<std::vector<int>> recv_off, recv_cnt;  // local ghost ranges

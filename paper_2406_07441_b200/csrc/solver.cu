@@ -201,6 +201,8 @@ struct Part {
     int rank = 0;  // partition index (= row of the reduction buffer)
     int n_pad = 0, n_owned = 0;
     std::vector<int> gs, oe, ge;
+    std::vector<int> ob;                 // per colour: end of the boundary owned points (LocalLayout::ob)
+    int n_btiles = 0;                    // leading tiles holding boundary points (overlapped exchanges)
     std::vector<int> perm;               // local -> global (-1 padding)
     std::vector<unsigned char> ghost;
     std::vector<int> own_gid, loc_gid;   // owned / owned+ghost global ids (compact transfers)
@@ -243,6 +245,25 @@ struct Solver::Impl {
     std::vector<Part> parts;
     std::vector<void*> owned;
     cudaStream_t s = nullptr;
+    // halo exchanges overlapped with the interior of their stage
+    // (partitioned transports on graphs; KF_OVERLAP=0: serialised): the
+    // exchange kernels / copies / NCCL calls go to xs, which is s2 between a
+    // fork and a join
+    bool overlap = false;
+    cudaStream_t s2 = nullptr, xs = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    void fork()
+    {
+        ck(cudaEventRecord(ev_fork, s), "fork");
+        ck(cudaStreamWaitEvent(s2, ev_fork, 0), "fork");
+        xs = s2;
+    }
+    void join()
+    {
+        ck(cudaEventRecord(ev_join, s2), "join");
+        ck(cudaStreamWaitEvent(s, ev_join, 0), "join");
+        xs = s;
+    }
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     // graph_iters consecutive iterations (cb, cb^1, ...) in one graph: the
     // first kernel of each iteration is a programmatic dependent of the
@@ -344,15 +365,19 @@ struct Solver::Impl {
         lc.numAttrs = pdl ? 1 : 0;
         ck(cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...), "launch");
     }
-    void launch_grad(Part& P, bool first, int src, int dst)
+    // tiles [t0, t1) of the gradient pass (t1 < 0: all)
+    void launch_grad(Part& P, bool first, int src, int dst, int t0 = 0, int t1 = -1)
     {
         if (gather) {
+            if (t1 < 0) t1 = P.n_tiles;
+            if (t1 <= t0) return;
             if (first)
-                launch(k_grad_t<true>, P.n_tiles, kTile, P.tile_smem1, P.D, src, dst);
+                launch(k_grad_t<true>, t1 - t0, kTile, P.tile_smem1, P.D, src, dst, t0);
             else
-                launch(k_grad_t<false>, P.n_tiles, kTile, P.tile_smem, P.D, src, dst);
+                launch(k_grad_t<false>, t1 - t0, kTile, P.tile_smem, P.D, src, dst, t0);
             return;
         }
+        if (t0 > 0) return;  // (global-gather kernels: one launch, no split)
         if (first)
             k_grad<true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, src, dst);
         else
@@ -420,6 +445,7 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         throw SolverError(KF_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
     ck(cudaSetDevice(cfg.device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    xs = s;
     n = c.n;
     if (c.n_colors > kMaxColors)
         throw SolverError(KF_CONFIG, "cloud needs " + std::to_string(c.n_colors) +
@@ -429,6 +455,15 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
     if (spec.n_parts < 1) throw SolverError(KF_CONFIG, "n_parts must be >= 1");
     n_rows = spec.n_parts;
     transport = spec.host ? kHost : spec.nccl ? kNccl : (spec.n_parts == 1 ? kSingle : kInProc);
+    {
+        const char* ov = std::getenv("KF_OVERLAP");
+        overlap = (transport == kInProc || transport == kNccl) && cfg.use_graph && !(ov && std::string(ov) == "0");
+        if (overlap) {
+            ck(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking), "cudaStreamCreate");
+            ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+        }
+    }
     if (transport == kHost) {
         if (!spec.exch || !spec.allreduce) throw SolverError(KF_CONFIG, "host transport needs exchange and allreduce");
         h_exch = spec.exch;
@@ -548,6 +583,9 @@ Solver::Impl::~Impl()
         if (P.hcomp) cudaFreeHost(P.hcomp);
     if (h_status) cudaFreeHost(h_status);
     if (h_iter) cudaFreeHost(h_iter);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (s2) cudaStreamDestroy(s2);
     if (s) cudaStreamDestroy(s);
 }
 
@@ -683,6 +721,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     P.gs = L.gs;
     P.oe = L.oe;
     P.ge = L.ge;
+    P.ob = L.ob;
     P.perm = L.perm;
     P.ghost = L.ghost;
     P.n_owned = L.n_owned;
@@ -958,6 +997,15 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                 if (P.perm[pn] >= 0) lc[pn] = code[P.perm[pn]];
             sort_by_key(own, lc);
         }
+        // overlapped exchanges: tiles of boundary points first (they alone
+        // read ghosts and feed the halo), the interior tiles after them
+        std::vector<char> isb;
+        if (overlap) {
+            isb.assign(n_pad, 0);
+            for (int g = 0; g < C; ++g)
+                for (int pn = P.gs[g]; pn < P.ob[g]; ++pn) isb[pn] = 1;
+            std::stable_partition(own.begin(), own.end(), [&](int pn) { return isb[pn] != 0; });
+        }
         if (!gather) own.clear();  // global-gather kernels: no tiles (one idle tile below)
         const char* to = std::getenv("KF_TILE_ORDER");
         const bool bfs = !(to && std::string(to) == "morton");
@@ -1062,6 +1110,11 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             }
         }
         const int n_tiles = static_cast<int>(tile_off.size()) - 1;
+        P.n_btiles = 0;
+        if (overlap)
+            for (int ti = 0; ti < n_tiles; ++ti)
+                for (int q = tile_off[ti]; q < tile_off[ti + 1]; ++q)
+                    if (isb[tile_pts[q]]) P.n_btiles = ti + 1;
         // -- content, one tile per task
         struct TileOut {
             std::vector<int> halo;
@@ -1547,9 +1600,9 @@ void Solver::Impl::post(Part& P, bool send, int peer, void* buf, size_t bytes)
     if (transport == kNccl) {
         const NcclApi& N = nccl();
         if (send)
-            nccl_check(N.Send(buf, bytes, ncclInt8, peer, comm, s), "ncclSend");
+            nccl_check(N.Send(buf, bytes, ncclInt8, peer, comm, xs), "ncclSend");
         else
-            nccl_check(N.Recv(buf, bytes, ncclInt8, peer, comm, s), "ncclRecv");
+            nccl_check(N.Recv(buf, bytes, ncclInt8, peer, comm, xs), "ncclRecv");
         return;
     }
     msgs.push_back(Msg{P.rank, peer, send, buf, bytes});
@@ -1625,7 +1678,7 @@ void Solver::Impl::flush_exchange()
             throw SolverError(KF_RUNTIME, "halo: message size mismatch " + std::to_string(snd.part) + " -> " +
                                               std::to_string(snd.peer));
         used[j] = 1;
-        ck(cudaMemcpyAsync(msgs[j].buf, snd.buf, snd.bytes, cudaMemcpyDeviceToDevice, s), "halo copy");
+        ck(cudaMemcpyAsync(msgs[j].buf, snd.buf, snd.bytes, cudaMemcpyDeviceToDevice, xs), "halo copy");
     }
     for (size_t j = 0; j < msgs.size(); ++j)
         if (!msgs[j].send && !used[j])
@@ -1638,7 +1691,7 @@ void Solver::Impl::exchange_rec(int slot)
 {
     for (Part& P : parts)
         if (P.n_send) {
-            k_pack_rec<<<blocks_for(8L * P.n_send, 256), 256, 0, s>>>(P.D.P[slot], P.d_send, P.n_send, P.sendP);
+            k_pack_rec<<<blocks_for(8L * P.n_send, 256), 256, 0, xs>>>(P.D.P[slot], P.d_send, P.n_send, P.sendP);
             mark("halo_pack");
         }
     begin_exchange();
@@ -1657,7 +1710,7 @@ void Solver::Impl::exchange_j(int c)
     for (Part& P : parts) {
         const int m = P.cstart[c + 1] - P.cstart[c];
         if (m) {
-            k_pack_j<<<blocks_for(8L * m, 256), 256, 0, s>>>(P.D.J, P.D.jbad, P.d_send + P.cstart[c], m,
+            k_pack_j<<<blocks_for(8L * m, 256), 256, 0, xs>>>(P.D.J, P.D.jbad, P.d_send + P.cstart[c], m,
                                                              P.sendJ + P.cstart[c], P.sendB + P.cstart[c]);
             mark("halo_pack");
         }
@@ -1708,41 +1761,81 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
             mark("q_from_u");
         }
     if (halo) exchange_rec(0);  // ghost q of this iteration
-    for (Part& P : parts) {
-        launch_grad(P, true, 0, 0);
-        mark("grad_pass1");
+    // Overlapped exchanges: the boundary tiles / points of a
+    // stage go first, the halo exchange of their results runs on s2 while
+    // the interior of the same stage runs on s, and the next stage joins.
+    // Only the boundary part reads ghosts or feeds the halo.
+    const bool ov = halo && overlap && gather;
+    auto grad_stage = [&](bool first, int src, int dst, int xslot) {
+        if (!ov) {
+            for (Part& P : parts) {
+                launch_grad(P, first, src, dst);
+                mark(first ? "grad_pass1" : "grad_passk");
+            }
+            exchange_rec(xslot);
+            return;
+        }
+        for (Part& P : parts) {
+            launch_grad(P, first, src, dst, 0, P.n_btiles);
+            mark(first ? "grad_pass1" : "grad_passk");
+        }
+        fork();
+        exchange_rec(xslot);
+        for (Part& P : parts) {
+            launch_grad(P, first, src, dst, P.n_btiles, P.n_tiles);
+            mark(first ? "grad_pass1" : "grad_passk");
+        }
+        join();
+    };
+    if (halo) {
+        grad_stage(true, 0, 0, 0);
+    } else {
+        for (Part& P : parts) {
+            launch_grad(P, true, 0, 0);
+            mark("grad_pass1");
+        }
     }
-    if (halo) exchange_rec(0);
     int slot = 0;
     for (int pass = 2; pass <= cfg.n_inner; ++pass) {
-        for (Part& P : parts) {
-            launch_grad(P, false, slot, slot ^ 1);
-            mark("grad_passk");
+        if (halo) {
+            grad_stage(false, slot, slot ^ 1, slot ^ 1);
+        } else {
+            for (Part& P : parts) {
+                launch_grad(P, false, slot, slot ^ 1);
+                mark("grad_passk");
+            }
         }
         slot ^= 1;
-        if (halo) exchange_rec(slot);
     }
     for (Part& P : parts) {
         launch_residual(P, slot);
         mark("flux_residual");
     }
+    // one colour of a sweep: [gs, ob) then [ob, oe) around the overlapped
+    // exchange of the colour's hoisted JVPs (xchg), or the whole block
+    auto sweep = [&](bool fwd, int c, bool xchg) {
+        auto go = [&](Part& P, int lo, int hi) {
+            if (hi <= lo) return;
+            if (fwd)
+                launch(k_forward, blocks_for(hi - lo, T), T, 0, P.D, cb, c, cfl_override, lo, hi);
+            else
+                launch(k_backward, blocks_for(hi - lo, T), T, 0, P.D, cb, c, lo, hi);
+            mark(fwd ? "lusgs_forward" : "lusgs_backward");
+        };
+        if (!(ov && xchg)) {
+            for (Part& P : parts) go(P, P.gs[c], P.oe[c]);
+            if (xchg) exchange_j(c);
+            return;
+        }
+        for (Part& P : parts) go(P, P.gs[c], P.ob[c]);
+        fork();
+        exchange_j(c);
+        for (Part& P : parts) go(P, P.ob[c], P.oe[c]);
+        join();
+    };
     if (parts[0].D.implicit) {
-        for (int c = 0; c < C; ++c) {
-            for (Part& P : parts) {
-                if (P.oe[c] == P.gs[c]) continue;  // no owned point of this colour here
-                launch(k_forward, blocks_for(P.oe[c] - P.gs[c], T), T, 0, P.D, cb, c, cfl_override);
-                mark("lusgs_forward");
-            }
-            if (halo && C > 1) exchange_j(c);
-        }
-        for (int c = C - 2; c >= 0; --c) {
-            for (Part& P : parts) {
-                if (P.oe[c] == P.gs[c]) continue;
-                launch(k_backward, blocks_for(P.oe[c] - P.gs[c], T), T, 0, P.D, cb, c);
-                mark("lusgs_backward");
-            }
-            if (halo && c > 0) exchange_j(c);
-        }
+        for (int c = 0; c < C; ++c) sweep(true, c, halo && C > 1);
+        for (int c = C - 2; c >= 0; --c) sweep(false, c, halo && c > 0);
     }
     for (Part& P : parts) {
         launch(k_update, blocks_for(P.n_pad, 256), 256, 0, P.D, cb, cfl_override);
@@ -2386,10 +2479,10 @@ int Solver::stage_lusgs(const double* U, const double* R, const double* dU_prev,
     D.S_out = d_S;
     for (int c = 0; c < I.C; ++c)
         if (Q.oe[c] > Q.gs[c])
-            k_forward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c, cfl);
+            k_forward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c, cfl, Q.gs[c], Q.oe[c]);
     for (int c = I.C - 2; c >= 0; --c)
         if (Q.oe[c] > Q.gs[c])
-            k_backward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c);
+            k_backward<<<blocks_for(Q.oe[c] - Q.gs[c], kThreads), kThreads, 0, I.s>>>(D, 0, c, Q.gs[c], Q.oe[c]);
     ck(cudaGetLastError(), "lusgs launch");
     auto grab1 = [&](double* h, const double* d) {
         if (!h) return;

@@ -99,6 +99,46 @@ def test_layouts_are_consistent_across_ranks(cloud, n_parts, mode):
                 assert np.all(owner[sent] == a) and np.all(colors[sent] == c + 1)
 
 
+@pytest.mark.parametrize("asym", [False, True])
+@pytest.mark.parametrize("n_parts", [2, 3])
+def test_layout_boundary_first(cloud, n_parts, asym):
+    """Inside each colour block the owned points a peer needs or that read a
+    ghost come first, [gs, ob); the interior [ob, oe) neither feeds nor reads
+    the halo, which is what lets the solver overlap the exchange with it --
+    also for asymmetric stencils (extra one-way neighbours)."""
+    c = cloud
+    if asym:
+        rng = np.random.default_rng(3)
+        nb = c.nbr
+        lists = [list(nb[p]) for p in range(c.n())]
+        inner = np.flatnonzero(c.kind == kf.PointKind.Interior)
+        for p in rng.choice(inner, 200, replace=False):
+            d = np.hypot(c.x - c.x[p], c.y - c.y[p])
+            q = int(np.argsort(d)[12])  # a one-way neighbour, two rings out
+            if q not in lists[p] and q != p:
+                lists[p].append(q)
+        off = np.zeros(c.n() + 1, np.int32)
+        np.cumsum([len(a) for a in lists], out=off[1:])
+        c = kf.PointCloud.from_arrays(c.x, c.y, c.kind.astype(np.int32), c.normal_x, c.normal_y, off,
+                                      np.concatenate(lists).astype(np.int32))
+    owner = kf.partition_plan(c, n_parts, "angular")
+    nb = c.nbr
+    for r in range(n_parts):
+        L = kf.LocalLayout(c, owner, n_parts, r)
+        sent = set()
+        for k in range(L.n_peers):
+            for cc in range(L.n_colors):
+                sent.update(L.send(k, cc).tolist())
+        for cc in range(L.n_colors):
+            assert L.gs[cc] <= L.ob[cc] <= L.oe[cc]
+            for pn in range(L.gs[cc], L.oe[cc]):
+                g = int(L.perm[pn])
+                if g < 0:
+                    continue
+                bnd = g in sent or any(owner[i] != r for i in nb[g])
+                assert bnd == (pn < L.ob[cc]), (r, cc, pn)
+
+
 def test_single_partition_layout_has_no_halo(cloud):
     L = kf.LocalLayout(cloud, np.zeros(cloud.n(), np.int32), 1, 0)
     assert L.n_peers == 0 and not L.ghost.any() and np.array_equal(L.oe, L.ge)
