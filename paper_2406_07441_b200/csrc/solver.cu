@@ -456,8 +456,14 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
     n_rows = spec.n_parts;
     transport = spec.host ? kHost : spec.nccl ? kNccl : (spec.n_parts == 1 ? kSingle : kInProc);
     {
+        // default: overlapped for the NCCL transport (one GPU per rank, the
+        // exchange crosses NVLink), serialised for in-process partitions on
+        // one device, where the copies compete with the interior for the
+        // same SMs and HBM (profiles/r02_overlap_inproc.txt: 1.246 vs 1.170
+        // ms at config 2); KF_OVERLAP=1 / 0 forces it on / off
         const char* ov = std::getenv("KF_OVERLAP");
-        overlap = (transport == kInProc || transport == kNccl) && cfg.use_graph && !(ov && std::string(ov) == "0");
+        const bool want = ov ? std::string(ov) != "0" : transport == kNccl;
+        overlap = want && (transport == kInProc || transport == kNccl) && cfg.use_graph;
         if (overlap) {
             ck(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking), "cudaStreamCreate");
             ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
@@ -1110,6 +1116,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             }
         }
         const int n_tiles = static_cast<int>(tile_off.size()) - 1;
+        lap("tile formation");
         P.n_btiles = 0;
         if (overlap)
             for (int ti = 0; ti < n_tiles; ++ti)
@@ -1244,6 +1251,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             }
         }
         if (!tile_error.empty()) throw SolverError(KF_CONFIG, tile_error);
+        lap("tile content");
         // -- concatenate
         for (int ti = 0; ti < n_tiles; ++ti) {
             twoff.push_back(twoff.back() + static_cast<long long>(outs[ti].nw));

@@ -150,3 +150,20 @@ def test_many_partitions_and_eager_launches(small, use_graph):
     assert len(r.iters) == len(one.iters) and r.abort_reason == one.abort_reason
     assert np.array_equal(r.final_state, one.final_state)
     assert relmax(r.residual, one.residual) <= 1e-13 and np.array_equal(r.cl, one.cl)
+
+
+@pytest.mark.parametrize("variant", ["manish_ad", "anandh", "explicit"])
+@pytest.mark.parametrize("n_parts,mode,nw,nr", [(4, "angular", 320, 120), (3, "morton", 96, 33)])
+def test_overlapped_exchanges_are_bitwise_single(monkeypatch, variant, n_parts, mode, nw, nr):
+    """KF_OVERLAP=1: every gradient pass and sweep colour runs its boundary
+    tiles / points first, exchanges their halo on a second stream while the
+    interior runs, and joins before the next stage (the NCCL transport's
+    default). States, histories and the abort record stay bitwise those of
+    the unpartitioned run."""
+    c = kf.generate_naca_ogrid("0012", nw, nr, 20.0)
+    one = kf.Solver(c, cfg(variant, n_iterations=40)).run(want_state=True)
+    monkeypatch.setenv("KF_OVERLAP", "1")
+    r = kf.Solver(c, cfg(variant, n_iterations=40), n_parts=n_parts, partition=mode).run(want_state=True)
+    assert len(r.iters) == len(one.iters) and r.abort_reason == one.abort_reason
+    assert np.array_equal(r.final_state, one.final_state)
+    assert np.array_equal(r.cl, one.cl) and relmax(r.residual, one.residual) <= 1e-13
