@@ -442,6 +442,12 @@ def main():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
+        if rank == 0:
+            # NCCL's communicator lines (nranks, NVLS / P2P transports) on
+            # rank 0's stderr, so the run's topology can be checked
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = spec_for(args.case, args.points)

@@ -659,7 +659,9 @@ kf_status kf_stage_forces(kf_ctx* ctx, const double* U, double* cl, double* cd)
 kf_status kf_probe_math(int n, int which, const double* x, double* lib, double* mine)
 {
     return guarded([&] {
-        if (which < 0 || which > 3) return err(KF_CONFIG, "which must be 0 (exp), 1 (log), 2 (erf) or 3 (division)");
+        if (which < 0 || which > 5)
+            return err(KF_CONFIG,
+                       "which must be 0 (exp), 1 (log), 2 (erf), 3 (division), 4 (erf polynomial) or 5 (exp(-t) polynomial)");
         kfb::probe_math(n, which, x, lib, mine);
         return ok();
     });
