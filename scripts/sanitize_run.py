@@ -25,4 +25,17 @@ s.reset(); s.iterate_async(2); U, dU = s.get_state(with_dU=True)
 outs = [np.zeros_like(U) for _ in range(3)]
 s.step_host_batch([U] * 3, [dU] * 3, outs, [np.zeros_like(U) for _ in range(3)])
 s.bench_mode(True); s.iterate_async(2); print("bench", s.sync_records()[1].code)
+# round 2: device colouring (Jones-Plassmann + iterated greedy) and the
+# wall-first levels, the overlapped exchanges (in-process, forced on), and a
+# cloud wide enough for many tiles (device-built weight streams)
+c2 = kf.generate_naca_ogrid("0012", 160, 41, 20.0)
+kf.color_points_device(c2, "ldf")
+kf.order_wall_first(c2)
+cfg = kf.SolverConfig(variant=kf.SolverVariant.ManishAD, mach_inf=0.63, aoa_deg=2.0, n_iterations=4)
+print("ordering variant", len(kf.Solver(c2, cfg).run().iters))
+os.environ["KF_OVERLAP"] = "1"
+for variant in ("manish_ad", "anandh"):
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(variant), mach_inf=0.63, aoa_deg=2.0, n_iterations=4)
+    print("overlap", variant, len(kf.Solver(kf.generate_naca_ogrid("0012", 160, 41, 20.0), cfg, n_parts=3).run().iters))
+os.environ.pop("KF_OVERLAP")
 print("done")
