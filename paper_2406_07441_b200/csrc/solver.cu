@@ -209,7 +209,8 @@ struct Part {
     Dev D{};
     int n_tile_blocks = 0, res_blocks = 0;
     int n_tiles = 0, nh_cap = 1, w_max = 0;
-    size_t tile_smem = 0, tile_smem1 = 0;  // dynamic SMEM of the staged kernels (pass >= 2 / residual, pass 1)
+    size_t tile_smem = 0, tile_smem1 = 0;  // dynamic SMEM of the staged kernels (residual / pass >= 2, pass 1)
+    size_t tile_smemk = 0;                 // passes >= 2 (5 units per record under KF_GRAD_G1)
     long long nnz_w = 0;
     // halo plan: peers (ascending rank); recv ranges [peer][colour] in local
     // numbering; send list colour-major, peer-minor: entries of (c, k) at
@@ -365,23 +366,28 @@ struct Solver::Impl {
         lc.numAttrs = pdl ? 1 : 0;
         ck(cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...), "launch");
     }
-    // tiles [t0, t1) of the gradient pass (t1 < 0: all)
-    void launch_grad(Part& P, bool first, int src, int dst, int t0 = 0, int t1 = -1)
+    // gradient pass `pass` (1 = first), tiles [t0, t1) (t1 < 0: all). The
+    // first-pass gradients a pass >= 2 needs (KF_GRAD_G1, kernels.cuh g1_of)
+    // come from its own source record (pass 2), its destination record
+    // (pass 3) or, for n_inner >= 4 only, an array the first pass stores.
+    void launch_grad(Part& P, int pass, int src, int dst, int t0 = 0, int t1 = -1)
     {
+        const bool first = pass == 1;
+        const int g1 = first ? (cfg.n_inner >= 4 ? 1 : 0) : pass == 2 ? 0 : pass == 3 ? 1 : 2;
         if (gather) {
             if (t1 < 0) t1 = P.n_tiles;
             if (t1 <= t0) return;
             if (first)
-                launch(k_grad_t<true>, t1 - t0, kTile, P.tile_smem1, P.D, src, dst, t0);
+                launch(k_grad_t<true>, t1 - t0, kTile, P.tile_smem1, P.D, src, dst, t0, g1);
             else
-                launch(k_grad_t<false>, t1 - t0, kTile, P.tile_smem, P.D, src, dst, t0);
+                launch(k_grad_t<false>, t1 - t0, kTile, P.tile_smemk, P.D, src, dst, t0, g1);
             return;
         }
         if (t0 > 0) return;  // (global-gather kernels: one launch, no split)
         if (first)
-            k_grad<true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, src, dst);
+            k_grad<true><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, src, dst, g1);
         else
-            k_grad<false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, src, dst);
+            k_grad<false><<<P.n_tile_blocks, kThreads, 0, s>>>(P.D, src, dst, g1);
     }
     void launch_residual(Part& P, int gslot)
     {
@@ -1444,6 +1450,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         const size_t ent_bytes = static_cast<size_t>(e_stride) * sizeof(unsigned short);
         P.tile_smem = static_cast<size_t>(kTileUnits) * P.nh_cap * sizeof(double2) + ent_bytes;
         P.tile_smem1 = static_cast<size_t>(3) * P.nh_cap * sizeof(double2) + ent_bytes;
+        P.tile_smemk = static_cast<size_t>(KF_GRAD_G1 ? 5 : kTileUnits) * P.nh_cap * sizeof(double2) + ent_bytes;
         if (P.tile_smem > kMaxTileSmem) throw SolverError(KF_CONFIG, "tile staging exceeds shared memory");
         // the attribute is per function (process-wide): never lower it below
         // what another context or partition launches with
@@ -1485,6 +1492,8 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             owned.erase(std::find(owned.begin(), owned.end(), static_cast<void*>(pos)));
         }
     }
+    // first-pass gradients for passes >= 4 (kernels.cuh g1_of)
+    D.G1 = KF_GRAD_G1 && cfg.n_inner >= 4 ? dalloc<double4>(2 * static_cast<size_t>(n_pad), owned) : nullptr;
     D.R = dalloc<double4>(n_pad, owned);
     D.dUs = dalloc<double4>(n_pad, owned);
     D.dU = dalloc<double4>(n_pad, owned);
@@ -1774,42 +1783,43 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
     // the interior of the same stage runs on s, and the next stage joins.
     // Only the boundary part reads ghosts or feeds the halo.
     const bool ov = halo && overlap && gather;
-    auto grad_stage = [&](bool first, int src, int dst, int xslot) {
+    auto grad_stage = [&](int pass, int src, int dst, int xslot) {
+        const char* nm = pass == 1 ? "grad_pass1" : "grad_passk";
         if (!ov) {
             for (Part& P : parts) {
-                launch_grad(P, first, src, dst);
-                mark(first ? "grad_pass1" : "grad_passk");
+                launch_grad(P, pass, src, dst);
+                mark(nm);
             }
             exchange_rec(xslot);
             return;
         }
         for (Part& P : parts) {
-            launch_grad(P, first, src, dst, 0, P.n_btiles);
-            mark(first ? "grad_pass1" : "grad_passk");
+            launch_grad(P, pass, src, dst, 0, P.n_btiles);
+            mark(nm);
         }
         fork();
         exchange_rec(xslot);
         for (Part& P : parts) {
-            launch_grad(P, first, src, dst, P.n_btiles, P.n_tiles);
-            mark(first ? "grad_pass1" : "grad_passk");
+            launch_grad(P, pass, src, dst, P.n_btiles, P.n_tiles);
+            mark(nm);
         }
         join();
     };
     if (halo) {
-        grad_stage(true, 0, 0, 0);
+        grad_stage(1, 0, 0, 0);
     } else {
         for (Part& P : parts) {
-            launch_grad(P, true, 0, 0);
+            launch_grad(P, 1, 0, 0);
             mark("grad_pass1");
         }
     }
     int slot = 0;
     for (int pass = 2; pass <= cfg.n_inner; ++pass) {
         if (halo) {
-            grad_stage(false, slot, slot ^ 1, slot ^ 1);
+            grad_stage(pass, slot, slot ^ 1, slot ^ 1);
         } else {
             for (Part& P : parts) {
-                launch_grad(P, false, slot, slot ^ 1);
+                launch_grad(P, pass, slot, slot ^ 1);
                 mark("grad_passk");
             }
         }
@@ -2422,10 +2432,10 @@ int Solver::stage_grads(const double* q, double* qx, double* qy)
     I.set_control(kNoKey, 0);
     I.upload_field(Q.D.P[0], 0, q);
     I.upload_field(Q.D.P[1], 0, q);
-    I.launch_grad(Q, true, 0, 0);
+    I.launch_grad(Q, 1, 0, 0);
     int slot = 0;
     for (int pass = 2; pass <= I.cfg.n_inner; ++pass) {
-        I.launch_grad(Q, false, slot, slot ^ 1);
+        I.launch_grad(Q, pass, slot, slot ^ 1);
         slot ^= 1;
     }
     I.download_field(qx, Q.D.P[slot], 1);

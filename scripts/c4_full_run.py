@@ -37,7 +37,11 @@ out = {"config": "naca0012:5120:1920:20 M0.63 AoA2 manish_ad CFL0.2", "points": 
        "first_order_equal": bool(np.array_equal(g.first_order[:n], r.first_order[:n])),
        "gpu_loop_seconds": g.loop_seconds, "ref_loop_seconds": r.loop_seconds,
        "gpu_wall_with_setup": t1 - t0, "ref_wall_with_setup": t2 - t1,
-       "decades_reached": float(np.log10(r.residual[0] / np.min(r.residual))) if n else None}
+       "decades_reached": float(np.log10(r.residual[0] / np.min(r.residual))) if n else None,
+       # per-iteration relative residual error (where a chaotic approach to
+       # the abort amplifies the few-ulp differences)
+       "residual_rel_per_iteration": [float(v) for v in np.abs(g.residual[:n] - r.residual[:n]) / np.abs(r.residual[:n])],
+       "gpu_residual": [float(v) for v in g.residual], "ref_residual": [float(v) for v in r.residual]}
 print(json.dumps(out))
 if len(sys.argv) > 1:
     with open(sys.argv[1], "w") as f:
