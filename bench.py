@@ -7,10 +7,12 @@ Workload (default: BASELINE.json configs[4], the largest single-GPU config,
 exact-AD JVPs (manish_ad), CFL 0.2, 3 inner gradient passes, physical BCs. A
 *step* is one fixed-point iteration (driver.cpp:218-276): q, 3 q-derivative
 passes, split-flux residual, time step + S-term + diagonal, 4 forward and 3
-backward colour sweeps, update + BCs, residual norm and CL/CD. Every timed
-step re-runs iteration 6 from the resident iteration-5 state (kf_bench_mode:
-the restart copy of U and dU_prev is inside the timed step), so each step is
-the same work; --case 2|3|4 selects the other BASELINE clouds.
+backward colour sweeps, update + BCs, residual norm and CL/CD. The timed
+steps are consecutive iterations of the run (after 5 + W warm-up iterations),
+like the reference arm's; cases whose reference run aborts within the timed
+window (configs 2 and 3) or --restart re-run iteration 6 from the resident
+iteration-5 state instead (kf_bench_mode: the restart copy of U and dU_prev
+inside every timed step). --case 2|3|4 selects the other BASELINE clouds.
 
   value : device-timed Mpoint-iter/s (CUDA events on the library stream,
           state resident in HBM), whole job over all ranks.
@@ -428,6 +430,9 @@ def main():
                     help="override the case's solver variant (evidence runs)")
     ap.add_argument("--ordering", type=int, default=1, choices=[0, 1, 2],
                     help="in-colour point order: 0 natural, 1 Morton (default), 2 reverse Cuthill-McKee")
+    ap.add_argument("--restart", action="store_true",
+                    help="time re-runs of iteration 6 from the iteration-5 state (bench mode) instead of "
+                         "consecutive iterations")
     ap.add_argument("--case", type=int, default=DEFAULT_CASE, choices=sorted(CASES),
                     help=f"BASELINE.json config whose cloud/case to time (default {DEFAULT_CASE})")
     args = ap.parse_args()
@@ -459,8 +464,13 @@ def main():
     t_gen = time.perf_counter() - t_setup
     N = cloud.n()
     colours = int(kf.color_points(cloud).n_colors)
+    # consecutive iterations unless the reference's own run aborts inside the
+    # window (configs 2 / 3 abort in iterations 22 / 7; the M 0.63 clouds
+    # run >= 116 iterations, profiles/r02_c4_fullrun.json)
+    n_window = WARM_ITERS + args.warmup + args.steps + 8
+    trajectory = not args.restart and args.case in (1, 4, 5) and n_window <= 100
     cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(spec["variant"]), mach_inf=spec["mach"],
-                          aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=64, device=local,
+                          aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=max(64, n_window), device=local,
                           ordering=args.ordering)
     t_create = time.perf_counter()
     if world > 1:
@@ -477,7 +487,8 @@ def main():
     # the resident iteration-5 state: every timed step (device and e2e) runs
     # iteration 6 from it
     U0, dU0 = solver.get_state(with_dU=True)
-    solver.bench_mode(True)
+    if not trajectory:
+        solver.bench_mode(True)
     stream = torch.cuda.ExternalStream(solver.stream_ptr, device=torch.device("cuda", local))
 
     if args.profile_only:
@@ -701,7 +712,9 @@ def main():
         "parallelism": (f"domain decomposition x{world} (angular wedges, NCCL halos), same cloud at every N"
                         if world > 1 else f"single-gpu, {args.parts} in-process partitions" if args.parts > 1
                         else "single-gpu"),
-        "step": "iteration 6 re-run from the resident iteration-5 state (restart copy inside the step)",
+        "step": (f"consecutive iterations {WARM_ITERS + args.warmup + 1}..{WARM_ITERS + args.warmup + args.steps} "
+                 "of the run (state resident in HBM)" if trajectory else
+                 "iteration 6 re-run from the resident iteration-5 state (restart copy inside the step)"),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                 "call": "kf_step_host_batch (C ABI, pinned host buffers; every step H2D(U, dU_prev) + "
                         "iteration + D2H(U', dU, record), copies of neighbouring steps overlapped); "
