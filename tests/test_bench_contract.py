@@ -56,3 +56,16 @@ def test_both_arms_print_the_same_config():
     c = kf.generate_naca_ogrid(spec["digits"], spec["n_wall"], spec["n_radial"], spec["radius"])
     assert line["config"] == bench.config_of(spec, bench.DEFAULT_CASE, c.n(), kf.color_points(c).n_colors)
     assert bench.DEFAULT_CASE == 5 and bench.CASES[5]["n_wall"] * bench.CASES[5]["n_radial"] == 40140800
+
+
+def test_multi_gpu_bench_is_strong_scaling_of_config5():
+    """bench.py --gpus N times the SAME config-5 cloud at every N (strong
+    scaling): the case does not depend on the world size."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import inspect
+    assert "world" not in inspect.signature(bench.spec_for).parameters
+    spec = bench.spec_for(bench.DEFAULT_CASE)
+    assert spec["n_wall"] * spec["n_radial"] == 40140800
+    src = inspect.getsource(bench.main)
+    assert '"strong" if world > 1' in src
