@@ -1122,6 +1122,24 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             }
         }
         const int n_tiles = static_cast<int>(tile_off.size()) - 1;
+        // lane order inside a tile (KF_TILE_LANES): bfs (formation order,
+        // default), id (the caller's numbering: on a structured cloud
+        // consecutive lanes then have consecutive neighbours, whose slots
+        // differ mod 8 -- fewer bank conflicts: gradient passes -6 %, but the
+        // flux kernel +5 % and the graph-launched iteration +10 % at config 5,
+        // profiles/r02_ab_tile_lanes.txt) or morton
+        {
+            const char* tl = std::getenv("KF_TILE_LANES");
+            const std::string lanes = tl ? tl : "bfs";
+            if (lanes == "id" || lanes == "morton") {
+                const bool by_id = lanes == "id";
+#pragma omp parallel for schedule(static)
+                for (int ti = 0; ti < n_tiles; ++ti)
+                    std::sort(tile_pts.begin() + tile_off[ti], tile_pts.begin() + tile_off[ti + 1], [&](int a, int b) {
+                        return by_id ? P.perm[a] < P.perm[b] : code[P.perm[a]] < code[P.perm[b]];
+                    });
+            }
+        }
         lap("tile formation");
         P.n_btiles = 0;
         if (overlap)

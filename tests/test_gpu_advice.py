@@ -71,3 +71,31 @@ def test_step_host_rejects_bad_buffers():
         s.step_host(U, dU, U_out=np.zeros((c.n(), 8))[:, ::2])
     out, rec = s.step_host(U.astype(np.float32).astype(np.float64), dU)  # converted inputs are fine
     assert out.shape == (c.n(), 4) and np.isfinite(rec.residual)
+
+
+def test_colour_limit_is_refused_at_create():
+    """The device sweeps take at most 120 colours (the abort key's 8-bit
+    stage field); a cloud whose greedy colouring needs more -- here a
+    121-point clique next to an O-grid -- is refused by kf_create with a
+    config error instead of running."""
+    base = kf.generate_naca_ogrid("0012", 48, 12, 12.0)
+    x, y, kind = list(base.x), list(base.y), list(base.kind)
+    nx, ny = list(base.normal_x), list(base.normal_y)
+    nb = base.nbr
+    lists = [list(nb.ids[nb.offsets[p]:nb.offsets[p + 1]]) for p in range(base.n())]
+    m, n0 = 121, base.n()
+    for k in range(m):
+        a = 2 * np.pi * k / m
+        x.append(30.0 + np.cos(a))
+        y.append(30.0 + np.sin(a))
+        kind.append(int(kf.PointKind.Interior))
+        nx.append(0.0)
+        ny.append(0.0)
+        lists.append([n0 + j for j in range(m) if j != k])
+    off = np.zeros(len(lists) + 1, np.int32)
+    np.cumsum([len(a) for a in lists], out=off[1:])
+    c = kf.PointCloud.from_arrays(np.array(x), np.array(y), np.array(kind, np.int32), np.array(nx), np.array(ny),
+                                  off, np.concatenate(lists).astype(np.int32))
+    assert kf.color_points(c).n_colors > 120
+    with pytest.raises(kf.ConfigError, match="at most 120"):
+        kf.Solver(c, kf.SolverConfig(variant=kf.SolverVariant.ManishAD, n_iterations=2))
