@@ -183,7 +183,7 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
     // for the send lists (points of `rank` that are ghosts of s)
     std::vector<std::vector<int>> send_to(n_parts);  // global ids owned here, ghost of s
     std::vector<int> my_ghosts;
-    {
+    if (n_parts > 1) {  // (one partition: no ghosts, nothing to send)
         for (int q = 0; q < c.n; ++q) {
             const int s = owner[q];
             for (int k = c.nbr.off[q]; k < c.nbr.off[q + 1]; ++k) {
@@ -207,6 +207,12 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
 
     // in-colour order of owned points (the single-GPU orders)
     std::vector<std::vector<int>> owned(C);
+    {
+        std::vector<int> cnt(C, 0);
+        for (int p = 0; p < c.n; ++p)
+            if (owner[p] == rank) ++cnt[col(p)];
+        for (int cc = 0; cc < C; ++cc) owned[cc].reserve(cnt[cc]);
+    }
     for (int p = 0; p < c.n; ++p)
         if (owner[p] == rank) owned[col(p)].push_back(p);
     if (ordering == 2) {
@@ -226,10 +232,12 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
         std::vector<char> sent(c.n, 0);
         for (const auto& v : send_to)
             for (int g : v) sent[g] = 1;
-        for (int p = 0; p < c.n; ++p)
-            if (owner[p] == rank)
-                for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1] && !sent[p]; ++k)
-                    if (owner[c.nbr.idx[k]] != rank) sent[p] = 1;
+        if (n_parts > 1)
+#pragma omp parallel for schedule(static)
+            for (int p = 0; p < c.n; ++p)
+                if (owner[p] == rank)
+                    for (int k = c.nbr.off[p]; k < c.nbr.off[p + 1] && !sent[p]; ++k)
+                        if (owner[c.nbr.idx[k]] != rank) sent[p] = 1;
         for (auto& m : owned) std::stable_partition(m.begin(), m.end(), [&](int p) { return sent[p] != 0; });
         L.ob.assign(C, 0);
         for (int cc = 0; cc < C; ++cc) {

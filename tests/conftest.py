@@ -13,6 +13,9 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# the device pack cross-checks every LS linear form against the stored
+# weight (bit for bit) in the test suite, a sample otherwise
+os.environ.setdefault("KF_VERIFY_FORMS", "1")
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
