@@ -270,6 +270,12 @@ LocalLayout build_local_layout(const Cloud& c, const std::vector<int>& owner, in
     L.oe.assign(C, 0);
     L.ge.assign(C, 0);
     std::vector<int> inv(c.n, -1);
+    {
+        size_t cap = my_ghosts.size() + 64 * static_cast<size_t>(C) + 32;
+        for (const auto& m : owned) cap += m.size();
+        L.perm.reserve(cap);
+        L.ghost.reserve(cap);
+    }
     for (int cc = 0; cc < C; ++cc) {
         L.gs[cc] = static_cast<int>(L.perm.size());
         L.ob[cc] += L.gs[cc];

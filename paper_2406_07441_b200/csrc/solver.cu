@@ -507,8 +507,12 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         const size_t worst = static_cast<size_t>(kTileUnits) * sizeof(double2) * (kHaloCap + 1 + 8 * 8) +
                              static_cast<size_t>(max_deg) * kTile * sizeof(unsigned short);
         if (worst > kMaxTileSmem) gather = 0;
+        // programmatic dependent launch pays on small clouds (config 2: 0.620
+        // -> 0.601 ms) and costs on large ones, whose next kernel's early CTAs
+        // take SM slots from the predecessor's tail (config 5: 30.5 -> 30.76
+        // ms; profiles/r02_ab_pdl.txt): on below 4M points; KF_PDL=0/1 forces
         const char* pe = std::getenv("KF_PDL");
-        pdl = !(pe && std::string(pe) == "0");
+        pdl = pe ? std::string(pe) != "0" : c.n < 4000000;
     }
     lap_ctor("device");
     std::vector<double> oty, otx;
@@ -746,25 +750,26 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     P.n_pad = static_cast<int>(P.perm.size());
     const int n_pad = P.n_pad;
     const int n_slices = n_pad / 32;
-    std::vector<int> inv(c.n, -1);
+    bvec<int> inv;
+    fresh(inv, c.n, -1);
+#pragma omp parallel for schedule(static)
+    for (int pn = 0; pn < n_pad; ++pn)
+        if (P.perm[pn] >= 0) inv[P.perm[pn]] = pn;
+    // compact transfers of a multi-process rank: owned / owned+ghost lists
     P.own_gid.clear();
     P.loc_gid.clear();
-    P.own_gid.reserve(n_pad);
-    P.loc_gid.reserve(n_pad);
     std::vector<int> own_loc, loc_loc;
-    own_loc.reserve(n_pad);
-    loc_loc.reserve(n_pad);
-    for (int pn = 0; pn < n_pad; ++pn) {
-        const int o = P.perm[pn];
-        if (o < 0) continue;
-        inv[o] = pn;
-        P.loc_gid.push_back(o);
-        loc_loc.push_back(pn);
-        if (!P.ghost[pn]) {
-            P.own_gid.push_back(o);
-            own_loc.push_back(pn);
+    if (per_rank())
+        for (int pn = 0; pn < n_pad; ++pn) {
+            const int o = P.perm[pn];
+            if (o < 0) continue;
+            P.loc_gid.push_back(o);
+            loc_loc.push_back(pn);
+            if (!P.ghost[pn]) {
+                P.own_gid.push_back(o);
+                own_loc.push_back(pn);
+            }
         }
-    }
 
     lap("renumber");
     // ---- per-point static data
@@ -866,7 +871,20 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         if (c.split[kYneg].degree(o)) ne |= 4;
         if (c.split[kYpos].degree(o)) ne |= 8;
         nonempty[pn] = ne;
-        // local_timestep's h (driver.cpp:33-36)
+        // local_timestep's h (driver.cpp:33-36) and the outer BC's nearest
+        // interior neighbour (driver.cpp:51-65) compare std::hypot values;
+        // the squared distances pre-select the candidates (a relative margin
+        // of 1e-12 covers every rounding of dx^2 + dy^2), so hypot runs on the
+        // near-minima only and the results are the reference's bit for bit
+        double d2min = std::numeric_limits<double>::infinity(), d2imin = d2min;
+        for (int k = c.nbr.off[o]; k < c.nbr.off[o + 1]; ++k) {
+            const int i = c.nbr.idx[k];
+            const double dx = c.x[i] - c.x[o], dy = c.y[i] - c.y[o];
+            const double d2 = dx * dx + dy * dy;
+            d2min = std::min(d2min, d2);
+            if (c.kind[i] == kInterior) d2imin = std::min(d2imin, d2);
+        }
+        const double lim = d2min * (1.0 + 1e-12), limi = d2imin * (1.0 + 1e-12);
         double h = std::numeric_limits<double>::max();
         int cnt[4] = {0, 0, 0, 0};
         int best = -1;
@@ -875,11 +893,15 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             const int i = c.nbr.idx[k];
             const double dx = c.x[i] - c.x[o];
             const double dy = c.y[i] - c.y[o];
-            const double dist = std::hypot(dx, dy);
-            h = std::min(h, dist);
-            if (c.kind[i] == kInterior && dist < best_d) {  // driver.cpp:51-65
-                best_d = dist;
-                best = i;
+            const double d2 = dx * dx + dy * dy;
+            const bool interior = c.kind[i] == kInterior;
+            if (d2 <= lim || (interior && d2 <= limi) || !(d2 == d2)) {
+                const double dist = std::hypot(dx, dy);
+                h = std::min(h, dist);
+                if (interior && dist < best_d) {  // driver.cpp:51-65
+                    best_d = dist;
+                    best = i;
+                }
             }
             // the linear forms must reproduce the stored weights bit for bit
             // (they are the reference's expression term for term; checked for
