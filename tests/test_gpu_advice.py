@@ -76,7 +76,7 @@ def test_step_host_rejects_bad_buffers():
 def test_colour_limit_is_refused_at_create():
     """The device sweeps take at most 120 colours (the abort key's 8-bit
     stage field); a cloud whose greedy colouring needs more -- here a
-    121-point clique next to an O-grid -- is refused by kf_create with a
+    121-point clique (far-field boundary points) next to an O-grid -- is refused by kf_create with a
     config error instead of running."""
     base = kf.generate_naca_ogrid("0012", 48, 12, 12.0)
     x, y, kind = list(base.x), list(base.y), list(base.kind)
@@ -84,12 +84,14 @@ def test_colour_limit_is_refused_at_create():
     nb = base.nbr
     lists = [list(nb.ids[nb.offsets[p]:nb.offsets[p + 1]]) for p in range(base.n())]
     m, n0 = 121, base.n()
+    rng = np.random.default_rng(5)  # a 2-D blob (no collinear split stencils)
     for k in range(m):
-        a = 2 * np.pi * k / m
-        x.append(30.0 + np.cos(a))
-        y.append(30.0 + np.sin(a))
-        kind.append(int(kf.PointKind.Interior))
-        nx.append(0.0)
+        x.append(30.0 + rng.uniform(-1, 1))
+        y.append(30.0 + rng.uniform(-1, 1))
+        # (boundary points: a blob's extreme points have one-point split
+        # stencils, singular -- refused for interior points, driver.cpp:198-201)
+        kind.append(int(kf.PointKind.Outer))
+        nx.append(1.0)
         ny.append(0.0)
         lists.append([n0 + j for j in range(m) if j != k])
     off = np.zeros(len(lists) + 1, np.int32)
