@@ -209,7 +209,9 @@ int jones_plassmann_colors(Cloud& c, int device, int mode, unsigned seed, int* r
     int* d_rem = nullptr;
     unsigned long long* d_prio = nullptr;
     unsigned char* d_win = nullptr;
+    int* d_new = nullptr;
     auto freeall = [&] {
+        cudaFree(d_new);
         cudaFree(d_off);
         cudaFree(d_adj);
         cudaFree(d_color);
@@ -266,7 +268,6 @@ int jones_plassmann_colors(Cloud& c, int device, int mode, unsigned seed, int* r
             ckc(cudaStreamSynchronize(s), "sync");
             nc = *std::max_element(h.begin(), h.end());
         }
-        int* d_new = nullptr;
         ckc(cudaMalloc(&d_new, sizeof(int) * n), "malloc");
         for (int pass = 0; pass < 4; ++pass) {
             ckc(cudaMemsetAsync(d_new, 0, sizeof(int) * n, s), "memset");
@@ -283,7 +284,6 @@ int jones_plassmann_colors(Cloud& c, int device, int mode, unsigned seed, int* r
             }
             nc = m;
         }
-        cudaFree(d_new);
         c.color.assign(n, 0);
         ckc(cudaMemcpyAsync(c.color.data(), d_color, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "D2H");
         ckc(cudaStreamSynchronize(s), "sync");
