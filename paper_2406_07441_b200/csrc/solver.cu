@@ -1022,6 +1022,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     // staged records; KF_TILE_ORDER=morton = plain Morton chunks. Content
     // (parallel over tiles): slots, 16-bit entries, weight stream.
     bvec<int> tpts, thalo;
+    bvec<unsigned short> town;  // staged slot of each lane's own record
     std::vector<int2> tmeta;
     int h_stride = 8, e_stride = kTile;
     bvec<unsigned short> tell;
@@ -1186,9 +1187,18 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         struct TileOut {
             std::vector<int> halo;
             std::vector<unsigned short> ent;
+            std::vector<unsigned short> own;  // staged slot of each lane's own record
             size_t nw = 0;
             int W = 0, ns = 0;
         };
+        // slot classes (KF_TILE_SLOTS): "free" (default) -- every staged
+        // record, the tile's own points included, takes the bank class
+        // (slot mod 8) that collides least with the other records its
+        // quarter-warps read in the same column (and, for own records, with
+        // the other own records of its quarter-warp); "lane" -- own point =
+        // slot lane, halo records classed around them (round 1)
+        const char* tsl = std::getenv("KF_TILE_SLOTS");
+        const bool free_slots = !(tsl && std::string(tsl) == "lane");
         std::vector<TileOut> outs(std::max(n_tiles, 0));
         std::string tile_error;
 #pragma omp parallel
@@ -1257,21 +1267,76 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                 int cls_count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 int ns = m;
                 std::vector<int> hslot(nh);
-                for (int h = 0; h < nh; ++h) {
-                    int best = 0, best_cost = 1 << 30;
-                    for (int b = 0; b < 8; ++b) {
-                        int cost = 0;
-                        for (int q = hstart[h]; q < hstart[h + 1]; ++q) cost += (gmask[order[q]] >> b) & 1;
-                        cost = cost * 4096 + cls_count[b];
-                        if (cost < best_cost) {
-                            best_cost = cost;
-                            best = b;
+                std::vector<int> oslot(m);
+                if (!free_slots) {
+                    for (int t = 0; t < m; ++t) oslot[t] = t;
+                    for (int h = 0; h < nh; ++h) {
+                        int best = 0, best_cost = 1 << 30;
+                        for (int b = 0; b < 8; ++b) {
+                            int cost = 0;
+                            for (int q = hstart[h]; q < hstart[h + 1]; ++q) cost += (gmask[order[q]] >> b) & 1;
+                            cost = cost * 4096 + cls_count[b];
+                            if (cost < best_cost) {
+                                best_cost = cost;
+                                best = b;
+                            }
                         }
+                        for (int q = hstart[h]; q < hstart[h + 1]; ++q) gmask[order[q]] |= static_cast<unsigned char>(1u << best);
+                        hslot[h] = base + 8 * cls_count[best] + best;
+                        ++cls_count[best];
+                        ns = std::max(ns, hslot[h] + 1);
                     }
-                    for (int q = hstart[h]; q < hstart[h + 1]; ++q) gmask[order[q]] |= static_cast<unsigned char>(1u << best);
-                    hslot[h] = base + 8 * cls_count[best] + best;
-                    ++cls_count[best];
-                    ns = std::max(ns, hslot[h] + 1);
+                } else {
+                    // groups of every record (own t: index t, halo h: m + h):
+                    // column groups kk * 16 + quarter-warp, self groups
+                    // W * 16 + quarter-warp (the own reads)
+                    const int QW = kTile / 8;
+                    std::vector<int> rg_start(m + nh + 1, 0), rg;
+                    std::vector<std::pair<int, int>> rgp;  // (record, group)
+                    rgp.reserve(static_cast<size_t>(m) * (W + 1) + pair_h.size());
+                    for (int t = 0; t < m; ++t) {
+                        rgp.emplace_back(t, W * QW + (t >> 3));
+                        const int o = P.perm[pts[t]];
+                        for (int kk = 0; kk < c.nbr.degree(o); ++kk) {
+                            const int v = find(inv[c.nbr.idx[c.nbr.off[o] + kk]]);
+                            rgp.emplace_back(v >= 0 ? v : m + (-2 - v), kk * QW + (t >> 3));
+                        }
+                        for (int kk = c.nbr.degree(o); kk < W; ++kk)  // padding entries read the own record
+                            rgp.emplace_back(t, kk * QW + (t >> 3));
+                    }
+                    for (const auto& pr : rgp) ++rg_start[pr.first + 1];
+                    for (int r = 0; r < m + nh; ++r) rg_start[r + 1] += rg_start[r];
+                    rg.assign(rgp.size(), 0);
+                    {
+                        std::vector<int> fill(rg_start.begin(), rg_start.end() - 1);
+                        for (const auto& pr : rgp) rg[fill[pr.first]++] = pr.second;
+                    }
+                    std::vector<unsigned char> gm(static_cast<size_t>(W + 1) * QW, 0);
+                    std::vector<int> rslot(m + nh);
+                    for (int r = 0; r < m + nh; ++r) {  // own records first, then the halo in first-use order
+                        int best = 0, best_cost = 1 << 30;
+                        for (int b = 0; b < 8; ++b) {
+                            int cost = 0;
+                            for (int q = rg_start[r]; q < rg_start[r + 1]; ++q) cost += (gm[rg[q]] >> b) & 1;
+                            cost = cost * 4096 + cls_count[b];
+                            if (cost < best_cost) {
+                                best_cost = cost;
+                                best = b;
+                            }
+                        }
+                        for (int q = rg_start[r]; q < rg_start[r + 1]; ++q) gm[rg[q]] |= static_cast<unsigned char>(1u << best);
+                        rslot[r] = 8 * cls_count[best] + best;
+                        ++cls_count[best];
+                    }
+                    ns = 0;
+                    for (int t = 0; t < m; ++t) {
+                        oslot[t] = rslot[t];
+                        ns = std::max(ns, oslot[t] + 1);
+                    }
+                    for (int h = 0; h < nh; ++h) {
+                        hslot[h] = rslot[m + h];
+                        ns = std::max(ns, hslot[h] + 1);
+                    }
                 }
                 if (ns > 4096) {
 #pragma omp critical(kf_tile_error)
@@ -1281,18 +1346,20 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
                 O.W = W;
                 O.ns = ns;
                 O.halo.assign(ns, pts[0]);  // unused class-grid slots stage a dummy record
-                for (int t = 0; t < m; ++t) O.halo[t] = pts[t];
+                for (int t = 0; t < m; ++t) O.halo[oslot[t]] = pts[t];
                 for (int h = 0; h < nh; ++h) O.halo[hslot[h]] = hid[h];
+                O.own.assign(kTile, 0);
+                for (int t = 0; t < m; ++t) O.own[t] = static_cast<unsigned short>(oslot[t]);
                 O.ent.assign(static_cast<size_t>(W) * kTile, 0);
                 for (int t = 0; t < m; ++t) {
                     const int o = P.perm[pts[t]];
                     const int deg = c.nbr.degree(o);
                     for (int kk = 0; kk < W; ++kk) {
-                        unsigned e = static_cast<unsigned>(t);  // padding: self, no split
+                        unsigned e = static_cast<unsigned>(oslot[t]);  // padding: own record, no split
                         if (kk < deg) {
                             const int k = c.nbr.off[o] + kk;
                             const int v = find(inv[c.nbr.idx[k]]);
-                            const int sl = v >= 0 ? v : hslot[-2 - v];
+                            const int sl = v >= 0 ? oslot[v] : hslot[-2 - v];
                             e = static_cast<unsigned>(sl) | (unsigned(emask[k]) << 12);
                         }
                         O.ent[static_cast<size_t>(kk) * kTile + t] = static_cast<unsigned short>(e);
@@ -1328,6 +1395,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         // + 2 rows of padding: the residual preloads two weights per entry
         tw_len = static_cast<size_t>(twoff.back()) + 2 * kTile;
         fresh(tpts, static_cast<size_t>(n_tiles) * kTile, -1);
+        fresh(town, tpts.size(), static_cast<unsigned short>(0));
         fresh(tlsf, tpts.size(), make_double4(0, 0, 0, 0));
         fresh(tlsfd, tpts.size(), make_double2(1, 1));
         fresh(tlsA, tpts.size(), make_double4(0, 0, 0, 0));
@@ -1338,6 +1406,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             std::copy(outs[ti].halo.begin(), outs[ti].halo.end(), thalo.begin() + static_cast<size_t>(ti) * h_stride);
             std::copy(outs[ti].ent.begin(), outs[ti].ent.end(), tell.begin() + static_cast<size_t>(ti) * e_stride);
             tmeta[ti] = make_int2(outs[ti].ns, outs[ti].W);
+            std::copy(outs[ti].own.begin(), outs[ti].own.end(), town.begin() + static_cast<size_t>(ti) * kTile);
             const int m = tile_off[ti + 1] - tile_off[ti];
             for (int t = 0; t < m; ++t) {
                 const int pn = tile_pts[tile_off[ti] + t];
@@ -1353,6 +1422,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         P.n_tiles = n_tiles;
         if (n_tiles == 0) {  // empty partition: one idle tile
             tpts.assign(kTile, -1);
+            town.assign(kTile, 0);
             tlsf.assign(kTile, make_double4(0, 0, 0, 0));
             tlsfd.assign(kTile, make_double2(1, 1));
             tlsA.assign(kTile, make_double4(0, 0, 0, 0));
@@ -1480,6 +1550,11 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
         D.nh_cap = P.nh_cap;
         D.w_max = P.w_max;
         D.t_pts = upi(tpts);
+        {
+            unsigned short* d_own = dalloc<unsigned short>(town.size(), owned);
+            up(d_own, town);
+            D.t_own = d_own;
+        }
         D.h_stride = h_stride;
         D.e_stride = e_stride;
         int2* d_meta = dalloc<int2>(tmeta.size(), owned);
