@@ -1191,14 +1191,16 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             size_t nw = 0;
             int W = 0, ns = 0;
         };
-        // slot classes (KF_TILE_SLOTS): "free" (default) -- every staged
-        // record, the tile's own points included, takes the bank class
-        // (slot mod 8) that collides least with the other records its
-        // quarter-warps read in the same column (and, for own records, with
-        // the other own records of its quarter-warp); "lane" -- own point =
-        // slot lane, halo records classed around them (round 1)
+        // slot classes (KF_TILE_SLOTS): "lane" (default) -- own point = slot
+        // lane, halo records take the bank class (slot mod 8) that collides
+        // least with the other records their quarter-warps read in the same
+        // column; "free" -- every staged record, own points included, is
+        // classed that way (the kernels read their own record through
+        // t_own). Measured (profiles/r02_ab_tile_slots.txt): conflicting
+        // wavefronts 41 -> 38 % in the gradient passes, 29 -> 34 % in the
+        // flux kernel, no time gained
         const char* tsl = std::getenv("KF_TILE_SLOTS");
-        const bool free_slots = !(tsl && std::string(tsl) == "lane");
+        const bool free_slots = tsl && std::string(tsl) == "free";
         std::vector<TileOut> outs(std::max(n_tiles, 0));
         std::string tile_error;
 #pragma omp parallel
