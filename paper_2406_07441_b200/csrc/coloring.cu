@@ -83,7 +83,9 @@ __global__ void k_jp_elect(int n, const long long* off, const int* adj, const un
     if (v >= n) return;
     win[v] = 0;
     if (color[v] != 0) return;
-    atomicAdd(remaining, 1);
+    // one atomic per warp: the still-uncoloured lanes are the active ones
+    const unsigned act = __activemask();
+    if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(remaining, __popc(act));
     const unsigned long long pv = prio[v];
     for (long long k = off[v]; k < off[v + 1]; ++k) {
         const int q = adj[k];
