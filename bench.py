@@ -649,6 +649,8 @@ def main():
         if trj and trj.get("points") == N and launches_key in trj.get("kernels", {}):
             o["traffic"] = float(trj["kernels"][launches_key]["dram_bytes"])
             o["traffic_over_alg"] = o["traffic"] / alg
+            if "fp64_pipe_active_pct" in trj["kernels"][launches_key]:
+                o["fp64_pipe_active_pct_ncu"] = trj["kernels"][launches_key]["fp64_pipe_active_pct"]
         return o
 
     flux = kernel_roof("flux_residual", FLUX_BYTES_FIXED + 4.0 * n_s, "flux_residual")
@@ -698,10 +700,13 @@ def main():
                 "roofline is `fp64`",
         "fp64": ({"achieved_tflops": flux["fp64_tflops"], "peak_tflops": fp64_peak, "frac": flux["fp64_frac"],
                   "flops_per_launch": flux["fp64_flops"],
+                  "pipe_active_pct_ncu": flux.get("fp64_pipe_active_pct_ncu"),
                   "how": "ncu 2 DFMA + DMUL + DADD thread instructions of one launch "
                          f"(profiles/r02_fp64_case{args.case}.json) / this run's CUDA-event kernel time; "
-                         "peak = measured DFMA loop (kf_measure_fp64_peak)"} if flux and "fp64_flops" in flux
-                 else None),
+                         "peak = measured DFMA loop (kf_measure_fp64_peak). The kernel's FP64 instruction "
+                         "count falls with every algorithmic saving (erf polynomial, log-free density), so "
+                         "the pipe activity (ncu, pipe_active_pct_ncu) is the utilisation measure"}
+                 if flux and "fp64_flops" in flux else None),
         "fp64_peak_tflops_measured": fp64_peak,
         "sweeps": sweeps,
         "gradients": {"pass1": g1, "passk": gk},

@@ -90,6 +90,9 @@ def traffic(rep, case, points):
     hdr, data = rows[0], rows[2:]
     ki = hdr.index("Kernel Name")
     rd, wr = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    pipe = hdr.index("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") \
+        if "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active" in hdr else None
+    dur = hdr.index("gpu__time_duration.sum")
     units = rows[1]
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     out = collections.OrderedDict()
@@ -102,9 +105,17 @@ def traffic(rep, case, points):
         e = out.setdefault(g, {"launches": 0, "dram_bytes": 0.0})
         e["launches"] += 1
         e["dram_bytes"] += b
+        if pipe is not None:  # FP64-pipe activity, time-weighted over the launches
+            t = float(d[dur].replace(",", ""))
+            e["_pipe_t"] = e.get("_pipe_t", 0.0) + t * float(d[pipe].replace(",", ""))
+            e["_t"] = e.get("_t", 0.0) + t
+    for e in out.values():
+        if "_t" in e:
+            e["fp64_pipe_active_pct"] = e.pop("_pipe_t") / e.pop("_t")
     res = {"case": case, "points": points, "kernels": out, "source": os.path.basename(rep),
            "how": "ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum summed over the launches of "
-                  "one iteration (cold-cache, serialised replays)"}
+                  "one iteration (cold-cache, serialised replays); fp64_pipe_active_pct = "
+                  "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active, time-weighted"}
     dst = os.path.join(ROOT, "profiles", f"r02_traffic_case{case}.json")
     with open(dst, "w") as f:
         json.dump(res, f, indent=1)
