@@ -60,3 +60,66 @@ def test_binary_cache_loads_faster_than_text(tmp_path):
     assert a.n() == b.n() == c.n()
     print(f"text {t1 - t0:.3f} s, binary {t2 - t1:.3f} s")
     assert (t2 - t1) < (t1 - t0)
+
+
+def _variants(tmp_path):
+    """Text clouds exercising the parser's edge cases: the reference's own
+    save_cloud output, CRLF line ends, comments and blank lines between
+    records, no final newline, and one malformed file per error path
+    (pointcloud.cpp:301-381)."""
+    import paper_2406_07441_b200 as kf
+    c = kf.generate_naca_ogrid("0012", 32, 8, 10.0)
+    good = tmp_path / "good.txt"
+    kf.save_cloud(c, good)
+    lines = good.read_text().splitlines()
+    out = {"good": "\n".join(lines) + "\n"}
+    out["crlf"] = "\r\n".join(lines) + "\r\n"
+    out["comments"] = "# cloud\n\n" + lines[0] + "\n" + "\n".join(
+        (f"   # c{k}\n\t\n" if k % 37 == 0 else "") + ln for k, ln in enumerate(lines[1:])) + "\n"
+    out["nofinalnl"] = "\n".join(lines)
+    out["badheader"] = "x\n" + "\n".join(lines[1:])
+    out["zeroheader"] = "0\n" + "\n".join(lines[1:])
+    out["order"] = "\n".join(lines[:5] + [lines[6], lines[5]] + lines[7:]) + "\n"
+    out["kind"] = "\n".join(lines[:9] + [" ".join(["9" if i == 3 else t for i, t in enumerate(lines[9].split())])]
+                            + lines[10:]) + "\n"
+    out["shortrec"] = "\n".join(lines[:11] + [" ".join(lines[11].split()[:3])] + lines[12:]) + "\n"
+    nb = lines[20].split()
+    out["missingnbr"] = "\n".join(lines[:20] + [" ".join(nb[:5 + int(nb[4]) - 1])] + lines[21:]) + "\n"
+    out["count"] = "\n".join(lines[:-1]) + "\n"
+    out["negnn"] = "\n".join(lines[:30] + [" ".join(lines[30].split()[:4] + ["-1"])] + lines[31:]) + "\n"
+    out["multi"] = "\n".join(lines[:7] + [lines[8], lines[7]] + lines[9:13] + ["junk"] + lines[14:]) + "\n"
+    out["range"] = out["good"].replace(lines[40], " ".join(
+        [t if i != 5 else "9999" for i, t in enumerate(lines[40].split())]))
+    out["self"] = out["good"].replace(lines[41], " ".join(
+        [t if i != 5 else lines[41].split()[0] for i, t in enumerate(lines[41].split())]))
+    return out
+
+
+def test_parallel_text_parser_matches_the_reference_loader(tmp_path):
+    """The parallel parser reads exactly what the reference's sequential
+    load_cloud reads, and fails on the same line with the same message."""
+    import paper_2406_07441_b200 as kf
+    from refpy import Reference, ref_available, OracleError
+    if not ref_available():
+        pytest.skip("reference not built")
+    for name, text in _variants(tmp_path).items():
+        path = tmp_path / f"{name}.txt"
+        path.write_bytes(text.encode())
+        try:
+            ref = Reference.load(path)
+            ref_err = None
+        except OracleError as e:
+            ref, ref_err = None, str(e)
+        try:
+            got = kf.load_cloud(path)
+            got_err = None
+        except kf.KinfreeError as e:
+            got, got_err = None, e.reason
+        assert (ref_err is None) == (got_err is None), (name, ref_err, got_err)
+        if ref_err is not None:
+            assert got_err == ref_err, (name, ref_err, got_err)
+            continue
+        x, y, kind, nx, ny = ref.geometry()
+        assert np.array_equal(got.x, x) and np.array_equal(got.y, y) and np.array_equal(got.kind, kind), name
+        off, idx = ref.csr(0)
+        assert np.array_equal(got.nbr.offsets, off) and np.array_equal(got.nbr.ids, idx), name
