@@ -446,10 +446,18 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args)
 
+    rank, world, local = dist_env()
+    lw = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if lw > 1 and (os.environ.get("OMP_NUM_THREADS") in (None, "1") and "KF_KEEP_OMP" not in os.environ):
+        # the ranks of a node build their partitions concurrently: split the
+        # host cores between them (torchrun's default of ONE thread per rank
+        # would make the 40M-point setup ~10x slower), set before the OpenMP
+        # runtime starts, i.e. before torch / the library load
+        ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or lw)
+        os.environ["OMP_NUM_THREADS"] = str(max(1, ncpu // lw))
     import torch
     import paper_2406_07441_b200 as kf
 
-    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         if rank == 0:
