@@ -373,7 +373,10 @@ struct Solver::Impl {
     void launch_grad(Part& P, int pass, int src, int dst, int t0 = 0, int t1 = -1)
     {
         const bool first = pass == 1;
-        const int g1 = first ? (cfg.n_inner >= 4 ? 1 : 0) : pass == 2 ? 0 : pass == 3 ? 1 : 2;
+        // (bit 2: carry q along, only into buffer 1 by the last pass, the
+        // buffer the flux kernel then stages q from; kernels.cuh k_grad_t)
+        const int g1 = (first ? (cfg.n_inner >= 4 ? 1 : 0) : pass == 2 ? 0 : pass == 3 ? 1 : 2) |
+                       (!first && dst == 1 && pass == cfg.n_inner ? 4 : 0);
         if (gather) {
             if (t1 < 0) t1 = P.n_tiles;
             if (t1 <= t0) return;

@@ -59,6 +59,18 @@ def test_partitioned_history_matches_single_and_reference(golden, small, variant
     assert np.max(np.abs(r.cl - h[variant + "_cl"])) <= 1e-10
 
 
+@pytest.mark.parametrize("n_inner", [1, 2, 4, 5])
+def test_partitioned_n_inner_is_bitwise_single(small, n_inner):
+    """Every gradient-pass count, partitioned vs single: the last pass of an
+    even count leaves the flux kernel's q in buffer 1 (carried there by that
+    pass, ghosts by the halo exchange), an odd count in buffer 0."""
+    one = kf.Solver(small, cfg("manish_ad", n_iterations=12, n_inner=n_inner)).run()
+    r = kf.Solver(small, cfg("manish_ad", n_iterations=12, n_inner=n_inner), n_parts=3).run()
+    assert len(r.iters) == len(one.iters) == 12, (r.abort_reason, one.abort_reason)
+    assert np.array_equal(r.final_state, one.final_state)
+    assert np.array_equal(r.cl, one.cl) and relmax(r.residual, one.residual) <= 1e-13
+
+
 def test_partitioned_state_is_bitwise_single_every_iteration(small):
     a = kf.Solver(small, cfg("manish_ad", n_iterations=20))
     b = kf.Solver(small, cfg("manish_ad", n_iterations=20), n_parts=4)
