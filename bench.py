@@ -65,7 +65,7 @@ DEFAULT_CASE = 5
 METRIC = "Mpoint-iter/s (FP64 LU-SGS+AD) and time-to-residual-drop, NACA 0012 clouds"
 UNIT = "Mpoint-iter/s"
 WARM_ITERS = 5
-E2E_MIN_STEPS = 32  # steps per pipelined host-fed call (see the e2e section)
+E2E_MIN_STEPS = 64  # steps per pipelined host-fed call (see the e2e section)
 # reference arm: iterations timed per run (13 s each on config 5 at 16 cores),
 # so the whole arm (46 s of reference setup included) ends in ~3 minutes
 REF_MAX_STEPS = 8
@@ -274,15 +274,59 @@ def run_reference_arm(args):
     return 0
 
 
-def pcie_ceiling(torch, n, step_ms, reps=3, rounds=4):
+class PinnedPool:
+    """Page-locked host buffers for the e2e copies: anonymous mmaps with
+    transparent huge pages, first touched by the filling copy and registered
+    with cudaHostRegister (2 MB pages: fewer IOMMU / page-table entries per
+    DMA; ~2-3 % more concurrent H2D+D2H than cudaHostAlloc's buffers on the
+    B200 box, profiles/r02_pcie_probe2.txt, and ~10x faster to pin).
+    torch.pin_memory() if registration fails."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.rt = torch.cuda.cudart()
+        self.held = []
+
+    def empty(self, shape, src=None):
+        import mmap
+        torch = self.torch
+        nb = int(np.prod(shape)) * 8
+        try:
+            m = mmap.mmap(-1, max(nb, 8), flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+            if hasattr(mmap, "MADV_HUGEPAGE"):
+                m.madvise(mmap.MADV_HUGEPAGE)
+            t = torch.frombuffer(m, dtype=torch.float64, count=int(np.prod(shape))).view(*shape)
+            if src is not None:
+                t.copy_(torch.from_numpy(np.ascontiguousarray(src)))
+            else:
+                t.zero_()
+            if int(self.rt.cudaHostRegister(t.data_ptr(), nb, 0)) != 0:
+                raise RuntimeError("cudaHostRegister")
+            self.held.append((t, m))
+            return t
+        except Exception:
+            t = torch.from_numpy(np.ascontiguousarray(src)) if src is not None else torch.empty(shape, dtype=torch.float64)
+            return t.pin_memory()
+
+    def release(self):
+        for t, m in self.held:
+            self.rt.cudaHostUnregister(t.data_ptr())
+        self.held = []
+
+
+def pcie_ceiling(torch, n, step_ms, reps=5, rounds=4, hin=None, hout=None):
     """The box's concurrent host<->device copy ceiling for one e2e step's
     bytes: H2D of (U, dU_prev) and D2H of (U', dU) on two streams, from and to
-    pinned buffers of the step's size, `rounds` steps' worth back to back per
-    timing (the sustained rate a pipelined run sees, not one cold burst),
-    timed with events (best of `reps`)."""
+    pinned buffers of the step's size (the e2e's own buffers when given),
+    `rounds` steps' worth back to back per timing (the sustained rate a
+    pipelined run sees, not one cold burst), timed with events (best of
+    `reps`)."""
     dev = torch.device("cuda")
-    hin = [torch.empty((n, 4), dtype=torch.float64).pin_memory() for _ in range(2)]
-    hout = [torch.empty((n, 4), dtype=torch.float64).pin_memory() for _ in range(2)]
+    pool = PinnedPool(torch)  # (the e2e's kind of buffer)
+    if hin is None:
+        hin = [pool.empty((n, 4)) for _ in range(2)]
+    if hout is None:
+        hout = [pool.empty((n, 4)) for _ in range(2)]
     din = [torch.empty((n, 4), dtype=torch.float64, device=dev) for _ in range(2)]
     dout = [torch.empty((n, 4), dtype=torch.float64, device=dev) for _ in range(2)]
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
@@ -310,13 +354,15 @@ def pcie_ceiling(torch, n, step_ms, reps=3, rounds=4):
             torch.cuda.synchronize()
             ts.append(max(e0.elapsed_time(e1), e0.elapsed_time(e2)) / rounds)
         best[mode] = min(ts)
+    del hin, hout
+    pool.release()
     bytes_dir = 2 * n * 32
     both = best["both"]
     return {"h2d_gbs": bytes_dir / best["h2d"] / 1e6, "d2h_gbs": bytes_dir / best["d2h"] / 1e6,
             "concurrent_ms_per_step": both,
             "bound_value": n / (max(both, step_ms) * 1e-3) / 1e6,
             "how": f"bare H2D of 2 x (n, 4) f64 and D2H of 2 x (n, 4) f64 per step on two streams from/to "
-                   f"pinned buffers, {rounds} steps back to back per timing (best of {reps}); bound = points / "
+                   f"pinned buffers (the e2e's), {rounds} steps back to back per timing (best of {reps}); bound = points / "
                    "max(copy time per step, device step time)"}
 
 
@@ -550,10 +596,11 @@ def main():
     local_cpus = gpu_local_cpus(local)
     if local_cpus:
         os.sched_setaffinity(0, local_cpus)
-    Uh = torch.from_numpy(U0).pin_memory()
-    dUh = torch.from_numpy(dU0).pin_memory()
-    Uo = torch.empty_like(Uh).pin_memory()
-    dUo = torch.empty_like(dUh).pin_memory()
+    pool = PinnedPool(torch)
+    Uh = pool.empty(U0.shape, U0)
+    dUh = pool.empty(dU0.shape, dU0)
+    Uo = pool.empty(U0.shape)
+    dUo = pool.empty(dU0.shape)
     del U0, dU0
     from paper_2406_07441_b200 import _lib
     rec = _lib.IterRecord()
@@ -577,8 +624,8 @@ def main():
     sync_ms = 1e3 * (time.perf_counter() - w0) / n_sync
     # pipelined form (kf_step_host_batch): the same steps, H2D of step k+1 and
     # D2H of step k-1 on the copy engines while step k computes
-    Uos = [torch.empty_like(Uh).pin_memory() for _ in range(2)]
-    dUos = [torch.empty_like(dUh).pin_memory() for _ in range(2)]
+    Uos = [pool.empty(tuple(Uh.shape)) for _ in range(2)]
+    dUos = [pool.empty(tuple(dUh.shape)) for _ in range(2)]
     # steps per pipelined call: the pipeline's fill and drain (the first
     # step's H2D, the last one's D2H: ~2 PCIe-bound step times) amortised
     # over at least E2E_MIN_STEPS steps, as a host feeding a long run would
@@ -620,8 +667,10 @@ def main():
     else:
         h2d_b = int(Uh.numel() * 8 + dUh.numel() * 8)
         d2h_b = int(Uo.numel() * 8 + dUo.numel() * 8 + C.sizeof(rec))
+    # the box's copy ceiling, timed on the same pinned pages
+    pcie = pcie_ceiling(torch, solver.owned_points if world > 1 else N, step_ms, hin=[Uh, dUh], hout=[Uo, dUo])
     del Uos, dUos, Uh, dUh, Uo, dUo
-    pcie = pcie_ceiling(torch, solver.owned_points if world > 1 else N, step_ms)
+    pool.release()
     pcie["frac"] = e2e_value / world / pcie["bound_value"] if world > 1 else e2e_value / pcie["bound_value"]
     if local_cpus:
         os.sched_setaffinity(0, full_aff)
