@@ -210,11 +210,11 @@ def _refpy():
     return refpy
 
 
-def reference_sample(spec, n_timed, threads):
+def reference_sample(spec, n_timed, threads, warm=1):
     """The reference solver (oracle/_ref, else the C restatement) on the case:
-    setup seconds, per-iteration seconds of iterations 2..n_timed+1 (runs
-    restarted from freestream before the reference's own aborts, iteration 1
-    of every run excluded), N, colours, kind."""
+    setup seconds, per-iteration seconds of iterations warm+1..warm+n_timed
+    (runs restarted from freestream before the reference's own aborts, the
+    first `warm` iterations of every run excluded), N, colours, kind."""
     refpy = _refpy()
     kind = "reference" if refpy.ref_available() else "port"
     t0 = time.perf_counter()
@@ -232,12 +232,13 @@ def reference_sample(spec, n_timed, threads):
     setup = time.perf_counter() - t0
     secs = []
     while len(secs) < n_timed:
-        m = min(n_timed - len(secs) + 1, 20)
+        m = min(n_timed - len(secs) + warm, 20)
         t1 = time.perf_counter()
         r = ctx.run(variant=spec["variant"], n_iterations=m, mach=spec["mach"], aoa_deg=spec["aoa"],
                     cfl=spec["cfl"])
         wall = time.perf_counter() - t1
-        s = list(r.seconds[1:]) if kind == "reference" else [wall / max(len(r.residual), 1)] * (len(r.residual) - 1)
+        s = (list(r.seconds[warm:]) if kind == "reference" else
+             [wall / max(len(r.residual), 1)] * max(len(r.residual) - warm, 0))
         if not s:
             break
         secs.extend(s)
@@ -253,15 +254,17 @@ def run_reference_arm(args):
     threads = cpu_cores()
     spec = spec_for(args.case, args.points)
     k = max(1, min(args.steps, REF_MAX_STEPS))
-    setup, secs, n, colours, kind = reference_sample(spec, k, threads)
+    warm = min(args.warmup, 3)  # (W >= 3 warm-up steps, bounded: 13 s each on config 5)
+    setup, secs, n, colours, kind = reference_sample(spec, k, threads, warm)
     total = float(np.sum(secs))
     value = n * len(secs) / total / 1e6
     sample = (f"{len(secs)} reference iterations of the same case and cloud (run_fixed_point through the "
-              f"reference's own API; iteration 1 of the run excluded as warm-up; at most {REF_MAX_STEPS} "
-              f"timed so the arm ends in minutes: the reference iteration is {total / len(secs):.1f} s)")
+              f"reference's own API; the run's first {warm} iterations excluded as warm-up; at most "
+              f"{REF_MAX_STEPS} timed so the arm ends in minutes: the reference iteration is "
+              f"{total / len(secs):.1f} s)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": len(secs), "warmup": 1, "ms_per_step": 1e3 * total / len(secs),
+        "steps": len(secs), "warmup": warm, "ms_per_step": 1e3 * total / len(secs),
         "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
         "config": config_of(spec, args.case, n, colours),
@@ -509,16 +512,26 @@ def main():
     import torch
     import paper_2406_07441_b200 as kf
 
+    # KF_BENCH_TRANSPORT=host (a test mode, never the default): the ranks
+    # exchange halos through the host-staged transport over gloo and may
+    # share one GPU, so the whole N > 1 bench path runs on a one-GPU box
+    # (NCCL refuses two ranks on one device)
+    host_tr = world > 1 and os.environ.get("KF_BENCH_TRANSPORT") == "host"
+    if host_tr:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        if rank == 0:
-            # NCCL's communicator lines (nranks, NVLS / P2P transports) on
-            # rank 0's stderr, so the run's topology can be checked
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if host_tr:
+            dist.init_process_group("gloo")
+        else:
+            if rank == 0:
+                # NCCL's communicator lines (nranks, NVLS / P2P transports) on
+                # rank 0's stderr, so the run's topology can be checked
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
+                os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = spec_for(args.case, args.points)
     if args.variant:
         spec["variant"] = args.variant
@@ -537,7 +550,20 @@ def main():
                           aoa_deg=spec["aoa"], cfl=spec["cfl"], n_iterations=max(64, n_window), device=local,
                           ordering=args.ordering)
     t_create = time.perf_counter()
-    if world > 1:
+    if host_tr:
+        def exchange(msgs):
+            reqs = []
+            for peer, is_send, buf in msgs:
+                t = torch.from_numpy(buf)
+                reqs.append(torch.distributed.isend(t, peer) if is_send else torch.distributed.irecv(t, peer))
+            for r in reqs:
+                r.wait()
+
+        def allreduce(buf):
+            torch.distributed.all_reduce(torch.from_numpy(buf))
+
+        solver = kf.Solver.for_rank_host(cloud, cfg, world, rank, exchange, allreduce)
+    elif world > 1:
         ids = [kf.nccl_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(ids, src=0)
         solver = kf.Solver.for_rank(cloud, cfg, world, rank, ids[0])
@@ -582,7 +608,8 @@ def main():
     recs, st = solver.sync_records()
     if st.code != 0:
         raise RuntimeError("benchmark iteration failed: " + st.reason.decode())
-    ms_t = torch.tensor([ms], device="cuda")
+    red_dev = "cpu" if host_tr else "cuda"  # (gloo reduces host tensors)
+    ms_t = torch.tensor([ms], device=red_dev)
     if world > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(ms_t.item())
@@ -651,7 +678,7 @@ def main():
         torch.cuda.synchronize()
         walls.append(1e3 * (time.perf_counter() - w0))
     e2e_ms = float(np.median(walls))
-    et = torch.tensor([e2e_ms, sync_ms * m_e2e], device="cuda")
+    et = torch.tensor([e2e_ms, sync_ms * m_e2e], device=red_dev)
     if world > 1:
         torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
     e2e_value = N * m_e2e / (float(et[0].item()) * 1e-3) / 1e6
@@ -661,14 +688,17 @@ def main():
     if world > 1:
         # each rank moves only its own (+ghost) points across PCIe
         n_loc = solver.owned_points
-        bt = torch.tensor([n_loc * 64, n_loc * 64 + C.sizeof(rec)], device="cuda", dtype=torch.int64)
+        bt = torch.tensor([n_loc * 64, n_loc * 64 + C.sizeof(rec)], device=red_dev, dtype=torch.int64)
         torch.distributed.all_reduce(bt)
         h2d_b, d2h_b = int(bt[0].item()), int(bt[1].item())
     else:
         h2d_b = int(Uh.numel() * 8 + dUh.numel() * 8)
         d2h_b = int(Uo.numel() * 8 + dUo.numel() * 8 + C.sizeof(rec))
     # the box's copy ceiling, timed on the same pinned pages
-    pcie = pcie_ceiling(torch, solver.owned_points if world > 1 else N, step_ms, hin=[Uh, dUh], hout=[Uo, dUo])
+    # (a rank moves only its owned points: the host arrays are whole-cloud
+    # sized, a prefix of that many rows stands in for them)
+    nl = solver.owned_points if world > 1 else N
+    pcie = pcie_ceiling(torch, nl, step_ms, hin=[Uh[:nl], dUh[:nl]], hout=[Uo[:nl], dUo[:nl]])
     del Uos, dUos, Uh, dUh, Uo, dUo
     pool.release()
     pcie["frac"] = e2e_value / world / pcie["bound_value"] if world > 1 else e2e_value / pcie["bound_value"]
@@ -785,7 +815,8 @@ def main():
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
         "config": config_of(spec, args.case, N, colours),
-        "parallelism": (f"domain decomposition x{world} (angular wedges, NCCL halos), same cloud at every N"
+        "parallelism": (f"domain decomposition x{world} (angular wedges, "
+                        f"{'host-staged gloo halos: TEST transport' if host_tr else 'NCCL halos'}), same cloud at every N"
                         if world > 1 else f"single-gpu, {args.parts} in-process partitions" if args.parts > 1
                         else "single-gpu"),
         "step": (f"consecutive iterations {WARM_ITERS + args.warmup + 1}..{WARM_ITERS + args.warmup + args.steps} "
@@ -812,7 +843,7 @@ def main():
     }
     del solver, cloud
     torch.cuda.empty_cache()
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # (the contract: rank 0 at N = 1 only)
         setup, secs, n_ref, _, kind = reference_sample(spec, 1, cpu_cores())
         line["cpu_baseline"] = {
             "value": n_ref * len(secs) / float(np.sum(secs)) / 1e6, "unit": UNIT, "cores": cpu_cores(),
