@@ -194,6 +194,131 @@ enum Transport : int { kSingle = 0, kInProc = 1, kNccl = 2, kHost = 3 };
 constexpr int kHaloCap = 6 * kTile - 1;
 constexpr size_t kMaxTileSmem = 200 * 1024;
 
+// Dataflow sweep schedule (kernels.cuh k_forward_df / k_backward_df): slice
+// colours, the handout orders and the dependency lists, from the sliced-ELL
+// entries the gathers read. Slice graph: slices a, b adjacent when a point of
+// one has a consumed (nonzero-weight) entry in the other. Levels: BFS over
+// the symmetric slice graph from a pseudo-peripheral slice (a second BFS from
+// the farthest slice of the first), per connected component. Adjacent slices
+// differ by at most one level, so forward key L + 2 c (backward (L_max - L) +
+// 2 (C - 1 - c)) puts every dependency (a lower- / higher-colour neighbour)
+// at a smaller key: the order is topological. Empty `ok` when a colour group
+// does not start and end on a slice boundary.
+struct DfHost {
+    bool ok = false;
+    int levels = 0;
+    std::vector<unsigned char> col;
+    std::vector<int> order_f, order_b, off_f, dep_f, off_b, dep_b;
+};
+
+DfHost build_df_schedule(int n_pad, int C, const std::vector<int>& gs, const std::vector<int>& ge,
+                         const std::vector<int>& slice_off, const unsigned* e_id)
+{
+    DfHost H;
+    const int ns = n_pad / 32;
+    if (ns == 0 || C < 1 || C > 250) return H;
+    H.col.assign(ns, 255);
+    for (int c = 0; c < C; ++c) {
+        if (gs[c] % 32 || ge[c] % 32) return H;
+        for (int sl = gs[c] / 32; sl < ge[c] / 32; ++sl) H.col[sl] = static_cast<unsigned char>(c);
+    }
+    for (int sl = 0; sl < ns; ++sl)
+        if (H.col[sl] == 255) return H;
+    // consumed neighbour slices of every slice (sorted, unique, without itself)
+    std::vector<int> noff(ns + 1, 0);
+    std::vector<std::vector<int>> nb(ns);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int sl = 0; sl < ns; ++sl) {
+        std::vector<int>& v = nb[sl];
+        for (int e = slice_off[sl]; e < slice_off[sl + 1]; ++e) {
+            const unsigned x = e_id[e];
+            if ((x >> 28) == 0) continue;
+            const int t = static_cast<int>((x & kIdMask) >> 5);
+            if (t != sl) v.push_back(t);
+        }
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+    }
+    // symmetric adjacency (CSR)
+    std::vector<int> deg(ns, 0);
+    for (int sl = 0; sl < ns; ++sl)
+        for (int t : nb[sl]) {
+            ++deg[sl];
+            ++deg[t];
+        }
+    std::vector<int> aoff(ns + 1, 0);
+    for (int sl = 0; sl < ns; ++sl) aoff[sl + 1] = aoff[sl] + deg[sl];
+    std::vector<int> adj(aoff[ns]);
+    std::vector<int> fill(aoff.begin(), aoff.end() - 1);
+    for (int sl = 0; sl < ns; ++sl)
+        for (int t : nb[sl]) {
+            adj[fill[sl]++] = t;
+            adj[fill[t]++] = sl;
+        }
+    // BFS levels per component from a pseudo-peripheral slice
+    std::vector<int> lev(ns, -1), q;
+    q.reserve(ns);
+    auto bfs = [&](int seed, std::vector<int>& L, std::vector<int>& comp) {
+        comp.clear();
+        L[seed] = 0;
+        comp.push_back(seed);
+        for (size_t h = 0; h < comp.size(); ++h) {
+            const int a = comp[h];
+            for (int k = aoff[a]; k < aoff[a + 1]; ++k)
+                if (L[adj[k]] < 0) {
+                    L[adj[k]] = L[a] + 1;
+                    comp.push_back(adj[k]);
+                }
+        }
+        return comp.back();
+    };
+    std::vector<int> tmp(ns, -1), comp;
+    for (int sl = 0; sl < ns; ++sl) {
+        if (lev[sl] >= 0) continue;
+        const int far = bfs(sl, tmp, comp);
+        bfs(far, lev, comp);
+    }
+    int lmax = 0;
+    for (int sl = 0; sl < ns; ++sl) lmax = std::max(lmax, lev[sl]);
+    H.levels = lmax + 1;
+    // handout orders: counting sort by key, slice id within a key
+    auto order_by = [&](auto key, auto take, std::vector<int>& out) {
+        const int nk = lmax + 2 * C + 1;
+        std::vector<int> cnt(nk + 1, 0);
+        for (int sl = 0; sl < ns; ++sl)
+            if (take(sl)) ++cnt[key(sl) + 1];
+        for (int k = 0; k < nk; ++k) cnt[k + 1] += cnt[k];
+        out.assign(cnt[nk], 0);
+        for (int sl = 0; sl < ns; ++sl)
+            if (take(sl)) out[cnt[key(sl)]++] = sl;
+    };
+    const int top = C - 1;
+    order_by([&](int sl) { return lev[sl] + 2 * H.col[sl]; }, [](int) { return true; }, H.order_f);
+    order_by([&](int sl) { return (lmax - lev[sl]) + 2 * (top - H.col[sl]); },
+             [&](int sl) { return H.col[sl] < top; }, H.order_b);
+    // dependency lists: forward the lower-colour slices read, backward the
+    // higher-colour ones below the top colour (the top colour's products come
+    // from the forward launch, complete before the backward one starts)
+    auto deps = [&](auto want, std::vector<int>& off, std::vector<int>& dep) {
+        off.assign(ns + 1, 0);
+        for (int sl = 0; sl < ns; ++sl) {
+            int k = 0;
+            for (int t : nb[sl]) k += want(sl, t) ? 1 : 0;
+            off[sl + 1] = off[sl] + k;
+        }
+        dep.assign(off[ns], 0);
+        for (int sl = 0; sl < ns; ++sl) {
+            int k = off[sl];
+            for (int t : nb[sl])
+                if (want(sl, t)) dep[k++] = t;
+        }
+    };
+    deps([&](int a, int b) { return H.col[b] < H.col[a]; }, H.off_f, H.dep_f);
+    deps([&](int a, int b) { return H.col[b] > H.col[a] && H.col[b] < top; }, H.off_b, H.dep_b);
+    H.ok = true;
+    return H;
+}
+
 }  // namespace
 
 // One partition's device layout and buffers.
@@ -235,6 +360,12 @@ struct Part {
     // reduction rows + cp (partitioned runs)
     double* red_local = nullptr;
     double* red = nullptr;
+    // dataflow sweeps (kernels.cuh k_forward_df): schedules, counters, flags
+    bool df = false;
+    int df_levels = 0;
+    DfSched dff{}, dfb{};
+    unsigned* df_ctl = nullptr;
+    unsigned* df_flag = nullptr;
 };
 
 struct Solver::Impl {
@@ -290,6 +421,7 @@ struct Solver::Impl {
     int W = 0;
     bool flux_exact = false;
     int sweep_threads = 32;
+    bool sweep_df = false;  // dataflow sweeps (large single-partition clouds)
     // two threads per point in the flux kernel (clouds of < KF_RES_SPLIT_MAX
     // points, default 200,000: a fraction of a wave of tiles, latency bound)
     bool res_split = false;  // residual kernel: libdevice-exact m3 (KF_FLUX_KERNEL=m3) or m4fast
@@ -516,6 +648,13 @@ Solver::Impl::Impl(const Cloud& c, const kf_config& cf, const PartitionSpec& spe
         // ms; profiles/r02_ab_pdl.txt): on below 4M points; KF_PDL=0/1 forces
         const char* pe = std::getenv("KF_PDL");
         pdl = pe ? std::string(pe) != "0" : c.n < 4000000;
+        // dataflow sweeps (one launch per sweep direction, slices in a
+        // level-skewed order meant to re-read the hoisted products from L2):
+        // measured slower at every size (config 5: forward + backward 8.64 ->
+        // 11.3 ms, DRAM reads up 12 %; profiles/r02_ab_dataflow_sweeps.txt),
+        // so opt-in only (KF_SWEEP_DF=1)
+        const char* dfe = std::getenv("KF_SWEEP_DF");
+        sweep_df = dfe && std::string(dfe) == "1";
     }
     lap_ctor("device");
     std::vector<double> oty, otx;
@@ -1509,6 +1648,36 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
     unsigned* d_eid = dalloc<unsigned>(n_e, owned);
     up(d_eid, e_id);
     D.e_id = d_eid;
+    // dataflow sweeps: one launch per sweep direction on large single-partition
+    // clouds (KF_SWEEP_DF=0/1 forces; kernels.cuh k_forward_df)
+    P.df = false;
+    if (transport == kSingle && cfg.variant != KF_EXPLICIT && sweep_df) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const DfHost H = build_df_schedule(n_pad, C, P.gs, P.ge, slice_off, e_id.data());
+        if (tm)
+            std::fprintf(stderr, "  pack %-14s %.2f s (%d slices, %d levels, %.2f / %.2f dependencies per slice)\n",
+                         "sweep schedule",
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(), n_slices,
+                         H.levels, H.ok ? double(H.dep_f.size()) / n_slices : 0.0,
+                         H.ok ? double(H.dep_b.size()) / n_slices : 0.0);
+        if (H.ok) {
+            auto upi = [&](const std::vector<int>& h) {
+                int* d = dalloc<int>(h.size(), owned);
+                up(d, h);
+                return static_cast<const int*>(d);
+            };
+            unsigned char* d_col = dalloc<unsigned char>(H.col.size(), owned);
+            up(d_col, H.col);
+            P.dff = DfSched{upi(H.order_f), upi(H.off_f), upi(H.dep_f), d_col, static_cast<int>(H.order_f.size())};
+            P.dfb = DfSched{upi(H.order_b), upi(H.off_b), upi(H.dep_b), d_col, static_cast<int>(H.order_b.size())};
+            // {ticket, -, epoch, spins (KF_DF_STATS builds)} then one flag per slice
+            P.df_ctl = dalloc<unsigned>(4 + static_cast<size_t>(n_slices), owned);
+            ck(cudaMemsetAsync(P.df_ctl, 0, sizeof(unsigned) * (4 + static_cast<size_t>(n_slices)), s), "memset");
+            P.df_flag = P.df_ctl + 4;
+            P.df_levels = H.levels;
+            P.df = true;
+        }
+    }
     double* d_sw[2];
     for (int dir = 0; dir < 2; ++dir) {
         const size_t len = std::max<size_t>(static_cast<size_t>(swoff[dir][n_slices]), 1);
@@ -1985,7 +2154,20 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
         for (Part& P : parts) go(P, P.ob[c], P.oe[c]);
         join();
     };
-    if (parts[0].D.implicit) {
+    if (parts[0].D.implicit && !halo && parts[0].df) {
+        Part& P = parts[0];
+        const int spb = kThreads / 32;  // slices per block
+        launch(k_df_reset, 1, 32, 0, P.df_ctl);  // (timed with the sweep it precedes)
+        ++launches;
+        launch(k_forward_df, (P.dff.n + spb - 1) / spb, kThreads, 0, P.D, cb, cfl_override, P.dff, P.df_ctl, P.df_flag);
+        mark("lusgs_forward");
+        if (C > 1) {
+            launch(k_df_reset, 1, 32, 0, P.df_ctl);
+            ++launches;
+            launch(k_backward_df, (P.dfb.n + spb - 1) / spb, kThreads, 0, P.D, cb, P.dfb, P.df_ctl, P.df_flag);
+            mark("lusgs_backward");
+        }
+    } else if (parts[0].D.implicit) {
         for (int c = 0; c < C; ++c) sweep(true, c, halo && C > 1);
         for (int c = C - 2; c >= 0; --c) sweep(false, c, halo && c > 0);
     }
