@@ -38,4 +38,10 @@ for variant in ("manish_ad", "anandh"):
     cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(variant), mach_inf=0.63, aoa_deg=2.0, n_iterations=4)
     print("overlap", variant, len(kf.Solver(kf.generate_naca_ogrid("0012", 160, 41, 20.0), cfg, n_parts=3).run().iters))
 os.environ.pop("KF_OVERLAP")
+# dataflow sweeps (KF_SWEEP_DF=1: ticketed blocks, per-slice release flags)
+os.environ["KF_SWEEP_DF"] = "1"
+for variant in ("manish_ad", "anandh"):
+    cfg = kf.SolverConfig(variant=kf.SolverVariant.parse(variant), mach_inf=0.63, aoa_deg=2.0, n_iterations=4)
+    print("dataflow", variant, len(kf.Solver(kf.generate_naca_ogrid("0012", 160, 41, 20.0), cfg).run().iters))
+os.environ.pop("KF_SWEEP_DF")
 print("done")
