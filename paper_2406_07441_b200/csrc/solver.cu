@@ -1670,7 +1670,7 @@ void Solver::Impl::pack(const Cloud& c, const LocalLayout& L, const std::vector<
             up(d_col, H.col);
             P.dff = DfSched{upi(H.order_f), upi(H.off_f), upi(H.dep_f), d_col, static_cast<int>(H.order_f.size())};
             P.dfb = DfSched{upi(H.order_b), upi(H.off_b), upi(H.dep_b), d_col, static_cast<int>(H.order_b.size())};
-            // {ticket, -, epoch, spins (KF_DF_STATS builds)} then one flag per slice
+            // {ticket, blocks done, epoch, spins (KF_DF_STATS builds)} then one flag per slice
             P.df_ctl = dalloc<unsigned>(4 + static_cast<size_t>(n_slices), owned);
             ck(cudaMemsetAsync(P.df_ctl, 0, sizeof(unsigned) * (4 + static_cast<size_t>(n_slices)), s), "memset");
             P.df_flag = P.df_ctl + 4;
@@ -2157,13 +2157,9 @@ void Solver::Impl::enqueue_iteration(int cb, double cfl_override, bool with_q)
     if (parts[0].D.implicit && !halo && parts[0].df) {
         Part& P = parts[0];
         const int spb = kThreads / 32;  // slices per block
-        launch(k_df_reset, 1, 32, 0, P.df_ctl);  // (timed with the sweep it precedes)
-        ++launches;
         launch(k_forward_df, (P.dff.n + spb - 1) / spb, kThreads, 0, P.D, cb, cfl_override, P.dff, P.df_ctl, P.df_flag);
         mark("lusgs_forward");
         if (C > 1) {
-            launch(k_df_reset, 1, 32, 0, P.df_ctl);
-            ++launches;
             launch(k_backward_df, (P.dfb.n + spb - 1) / spb, kThreads, 0, P.D, cb, P.dfb, P.df_ctl, P.df_flag);
             mark("lusgs_backward");
         }
