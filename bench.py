@@ -265,7 +265,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(secs), "warmup": warm, "ms_per_step": 1e3 * total / len(secs),
-        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
         "config": config_of(spec, args.case, n, colours),
         "parallelism": f"cpu-openmp ({threads} host threads)",
@@ -813,7 +813,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated NACA 0012 O-grid, deterministic; no RNG)",
         "config": config_of(spec, args.case, N, colours),
         "parallelism": (f"domain decomposition x{world} (angular wedges, "
