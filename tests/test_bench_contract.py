@@ -68,4 +68,4 @@ def test_multi_gpu_bench_is_strong_scaling_of_config5():
     spec = bench.spec_for(bench.DEFAULT_CASE)
     assert spec["n_wall"] * spec["n_radial"] == 40140800
     src = inspect.getsource(bench.main)
-    assert '"strong" if world > 1' in src
+    assert '"scaling": "strong",' in src
